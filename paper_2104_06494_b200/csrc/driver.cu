@@ -1,0 +1,587 @@
+// The PAGANI iteration (Alg. 2) on one B200: host C++ makes every scalar
+// decision exactly as /root/reference/proj/src/driver.cpp:83-215 does; the
+// region list never leaves HBM.  Per iteration:
+//
+//   k_evaluate  (rule + two-level refine + rel-err classify, fused)
+//   k_fold_eval (serial 2048-block partials of est, err, finished est/err,
+//                active counts)  ->  k_finalize (pairwise trees, offsets)
+//   -- one 48-byte D2H of the scalars, host decisions --
+//   [threshold search: k_minmax, then per probe k_probe -> k_finalize -> D2H]
+//   k_split     (fused filter + bisect into the other buffer)
+//
+// Host arithmetic is compiled with -ffp-contract=off and uses the same
+// expression order as the reference, so v, e, v_f, e_f, budgets and
+// thresholds are bit-identical (tests/test_gpu_parity.py compares every
+// per-iteration trace field with the reference library).
+#include "driver.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+
+namespace pgn {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Workspace
+void Workspace::ensure(int n_, int64_t cap_) {
+  cap_ = ((cap_ + kBlock - 1) / kBlock) * kBlock;
+  if (cap_ <= cap && n_ <= n) return;
+  PGN_CK(cudaSetDevice(device));
+  const int64_t nc = cap_ > cap ? cap_ : cap;
+  const int nn = n_ > n ? n_ : n;
+  const int64_t nb = nc / kBlock;
+  for (int b = 0; b < 2; ++b) {
+    low[b].alloc(static_cast<size_t>(nn) * nc);
+    len[b].alloc(static_cast<size_t>(nn) * nc);
+  }
+  pest.alloc(nc);
+  est.alloc(nc);
+  err.alloc(nc);
+  axis.alloc(nc);
+  flag.alloc(nc);
+  flag2.alloc(nc);
+  part_eval.alloc(4 * nb);
+  part_probe.alloc(4 * nb);
+  scratch.alloc(2 * nb + 2);
+  cnt_eval.alloc(nb);
+  cnt_probe.alloc(nb);
+  off_eval.alloc(nb);
+  off_probe.alloc(nb);
+  if (!d_sc.p) {
+    d_sc.alloc(2);
+    mm_keys.alloc(2);
+    mm_out.alloc(2);
+    d_lower.alloc(16);
+    d_step.alloc(16);
+    d_tmp.alloc(4);
+    PGN_CK(cudaMallocHost(&h_sc, 2 * sizeof(FoldScalars)));
+    PGN_CK(cudaMallocHost(&h_mm, 4 * sizeof(double)));
+  }
+  n = nn;
+  cap = nc;
+  nblk_cap = nb;
+}
+
+cudaEvent_t Workspace::event(size_t i) {
+  while (ev.size() <= i) {
+    cudaEvent_t e;
+    PGN_CK(cudaEventCreate(&e));
+    ev.push_back(e);
+  }
+  return ev[i];
+}
+
+Workspace::~Workspace() {
+  for (auto e : ev) cudaEventDestroy(e);
+  if (h_sc) cudaFreeHost(h_sc);
+  if (h_mm) cudaFreeHost(h_mm);
+  if (st) cudaStreamDestroy(st);
+}
+
+namespace {
+std::mutex g_ws_mu;
+std::map<int, std::unique_ptr<Workspace>>& ws_map() {
+  static std::map<int, std::unique_ptr<Workspace>> m;
+  return m;
+}
+}  // namespace
+
+Workspace& workspace_for(int device) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  auto& m = ws_map();
+  auto it = m.find(device);
+  if (it != m.end()) return *it->second;
+  int count = 0;
+  PGN_CK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) throw CudaError("no CUDA device " + std::to_string(device));
+  auto ws = std::make_unique<Workspace>();
+  ws->device = device;
+  PGN_CK(cudaSetDevice(device));
+  PGN_CK(cudaStreamCreateWithFlags(&ws->st, cudaStreamNonBlocking));
+  Workspace& r = *ws;
+  m[device] = std::move(ws);
+  return r;
+}
+
+void release_workspaces() {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  ws_map().clear();
+}
+
+// ---------------------------------------------------------------------------
+// Integrand resolution: the device has no CPU fallback.
+DeviceIntegrand resolve_integrand(const pagani_integrand* f) {
+  if (!f) throw std::invalid_argument("integrand is null");
+  if (f->magic != PAGANI_INTEGRAND_MAGIC)
+    throw std::invalid_argument("integrand: bad magic (use pagani_integrand_builtin)");
+  if (f->kind == PAGANI_HOST_FN)
+    throw UnsupportedError(
+        "host function-pointer integrands cannot run on the GPU (no CPU fallback); "
+        "use a builtin integrand");
+  if (f->kind != PAGANI_BUILTIN) throw std::invalid_argument("integrand: unknown kind");
+  const int id = f->builtin_id;
+  const bool ok = (id >= 1 && id <= 8) || (id >= 100 && id <= 106);
+  if (!ok) throw std::invalid_argument("unknown integrand id " + std::to_string(id));
+  DeviceIntegrand d;
+  d.fid = id;
+  const int np = f->n_params < 0 ? 0 : (f->n_params > 32 ? 32 : f->n_params);
+  for (int i = 0; i < np; ++i) d.params.p[i] = f->params[i];
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Scalar helpers (driver.cpp:28-58)
+int convergence_digits(double tau_rel) {
+  const double d = std::ceil(std::log10(1.0 / tau_rel));
+  if (!(d >= 1.0)) return 1;
+  if (d > 17.0) return 17;
+  return static_cast<int>(d);
+}
+
+bool digits_converged(double v_prev, double v_curr, int digits) {
+  if (!std::isfinite(v_prev) || !std::isfinite(v_curr)) return false;
+  if (v_prev == 0.0 && v_curr == 0.0) return true;
+  if ((v_prev < 0.0) != (v_curr < 0.0)) return false;
+  if (digits < 1) digits = 1;
+  if (digits > 17) digits = 17;
+  char a[40], b[40];
+  std::snprintf(a, sizeof a, "%.*e", digits - 1, v_prev);
+  std::snprintf(b, sizeof b, "%.*e", digits - 1, v_curr);
+  return std::strcmp(a, b) == 0;
+}
+
+int initial_subdivisions(int n, int64_t init_target) {  // geometry.cpp:67-81
+  int d = 1;
+  for (;;) {
+    int64_t p = 1;
+    bool over = false;
+    for (int a = 0; a < n; ++a) {
+      if (p > init_target / (d + 1)) {
+        over = true;
+        break;
+      }
+      p *= d + 1;
+    }
+    if (over || p > init_target) break;
+    ++d;
+  }
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Threshold search (classify.cpp:37-95) with device probes.
+ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
+                                  const double* d_err, const uint8_t* d_flag, double v_tot,
+                                  double e_tot, double e_it, int64_t s_it, double tau_rel,
+                                  const Limits& lim, double* probe_ms) {
+  ThresholdOutcome r;
+  if (s_it <= 0) return r;
+  const double e_budget = e_tot - std::fabs(v_tot) * tau_rel;
+  double p_max = lim.p_max_start;
+  r.budget_limit = p_max * e_budget;
+  if (!(e_budget > 0.0)) return r;
+
+  cudaStream_t st = ws.st;
+  launch_minmax(st, m, d_err, ws.mm_keys.p, ws.mm_out.p);
+  PGN_CK(cudaMemcpyAsync(ws.h_mm, ws.mm_out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PGN_CK(cudaStreamSynchronize(st));
+  const double min_err = ws.h_mm[0], max_err = ws.h_mm[1];
+  double t = e_it / static_cast<double>(s_it);
+
+  enum Dir { kNone, kTowardMax, kTowardMin };
+  Dir last = kNone;
+  const int64_t nblk = nblocks_of(m);
+  while (r.attempts < lim.attempt_limit) {
+    ++r.attempts;
+    cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
+    if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
+    launch_probe(st, m, t, d_est, d_err, d_flag, ws.part_probe.p, ws.cnt_probe.p);
+    launch_finalize(st, nblk, 2, ws.part_probe.p, ws.cnt_probe.p, ws.off_probe.p, ws.scratch.p,
+                    ws.d_sc.p + 1);
+    if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
+    PGN_CK(cudaMemcpyAsync(ws.h_sc + 1, ws.d_sc.p + 1, sizeof(FoldScalars),
+                           cudaMemcpyDeviceToHost, st));
+    PGN_CK(cudaStreamSynchronize(st));
+    if (probe_ms) {
+      float ms = 0;
+      PGN_CK(cudaEventElapsedTime(&ms, e0, e1));
+      *probe_ms += ms;
+    }
+    const FoldScalars sc = ws.h_sc[1];
+    const int64_t inactive = s_it - sc.count;
+    const bool memory_ok = 2 * inactive > s_it;
+    const double discarded = sc.sum[0];
+    if (memory_ok && discarded <= p_max * e_budget) {
+      r.success = true;
+      r.threshold = t;
+      r.discarded = discarded;
+      r.budget_limit = p_max * e_budget;
+      r.finished_count = inactive;
+      r.fin_v = sc.sum[1];
+      return r;
+    }
+    const Dir dir = memory_ok ? kTowardMin : kTowardMax;
+    if (last != kNone && dir != last) {
+      ++r.direction_changes;
+      if (r.direction_changes > lim.direction_change_limit) break;
+      const double stepped = p_max + lim.p_max_step;
+      p_max = (stepped < lim.p_max_cap) ? stepped : lim.p_max_cap;  // std::min(cap, p+step)
+    }
+    last = dir;
+    t = dir == kTowardMax ? (t + max_err) * 0.5 : (t + min_err) * 0.5;
+  }
+  r.threshold = t;
+  r.budget_limit = p_max * e_budget;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Bounds {
+  std::vector<double> lower, upper;
+};
+
+void validate_bounds(int n, const double* lower, const double* upper) {  // geometry.cpp:9-23
+  if (!lower || !upper) throw std::invalid_argument("Bounds: lower/upper size mismatch");
+  if (n < 1 || n > kMaxDim)
+    throw std::invalid_argument("Bounds: dimension must be in [1, 16]");
+  for (int a = 0; a < n; ++a) {
+    if (!(lower[a] < upper[a]))
+      throw std::invalid_argument("Bounds: lower must be < upper on every axis");
+    if (!std::isfinite(lower[a]) || !std::isfinite(upper[a]))
+      throw std::invalid_argument("Bounds: entries must be finite");
+  }
+}
+
+void validate_config(const pagani_config& c) {  // driver.cpp:35-41
+  if (!(c.tau_rel > 0.0)) throw std::invalid_argument("Config: tau_rel must be > 0");
+  if (!(c.tau_abs >= 0.0)) throw std::invalid_argument("Config: tau_abs must be >= 0");
+  if (c.it_max < 1) throw std::invalid_argument("Config: it_max must be >= 1");
+  if (c.init_subdiv == 0 && c.max_regions < 2 * c.init_target)
+    throw std::invalid_argument("Config: max_regions must be >= 2 * init_target");
+}
+
+struct KTimer {
+  Workspace& ws;
+  bool on;
+  std::vector<std::pair<int, std::pair<size_t, size_t>>> spans;
+  size_t next = 2;  // events 0/1 belong to the probe loop
+  KTimer(Workspace& w, bool o) : ws(w), on(o) {}
+  size_t mark() {
+    if (!on) return 0;
+    const size_t i = next++;
+    PGN_CK(cudaEventRecord(ws.event(i), ws.st));
+    return i;
+  }
+  void span(int slot, size_t a, size_t b) {
+    if (on) spans.push_back({slot, {a, b}});
+  }
+  void collect(pagani_result* out) {
+    if (!on) return;
+    for (auto& s : spans) {
+      float ms = 0;
+      PGN_CK(cudaEventElapsedTime(&ms, ws.event(s.second.first), ws.event(s.second.second)));
+      out->kernel_ms[s.first] += ms;
+    }
+    spans.clear();
+    next = 2;
+  }
+};
+
+}  // namespace
+
+void integrate(const pagani_integrand* f, int ndim, const double* lower, const double* upper,
+               const pagani_config* cfg_in, pagani_result* out) {
+  const auto t_wall0 = std::chrono::steady_clock::now();
+  if (!cfg_in || !out) throw std::invalid_argument("null config or result");
+  const pagani_config cfg = *cfg_in;
+  validate_config(cfg);
+  validate_bounds(ndim, lower, upper);
+  const int n = ndim;
+  const DeviceIntegrand di = resolve_integrand(f);
+  if (cfg.mode != PAGANI_MODE_PARITY && cfg.mode != PAGANI_MODE_FAST)
+    throw std::invalid_argument("Config: unknown mode");
+  const EvalKernel eval_k = lookup_evaluate(di.fid, n, cfg.mode);
+  if (!eval_k) throw UnsupportedError("no device kernel for this integrand/dimension");
+  if (cfg.comm) throw UnsupportedError("multi-GPU communicator passed to the 1-GPU driver");
+
+  std::memset(out, 0, sizeof(*out));
+  Workspace& ws = workspace_for(cfg.device);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  PGN_CK(cudaSetDevice(ws.device));
+  cudaStream_t st = ws.st;
+
+  // driver.cpp:92-99 -- work on the unit cube, scale at the end.
+  bool mapped = false;
+  double jacobian = 1.0;
+  double dom_len[kMaxDim];
+  for (int a = 0; a < n; ++a) {
+    if (lower[a] != 0.0 || upper[a] != 1.0) mapped = true;
+    jacobian *= upper[a] - lower[a];
+    dom_len[a] = upper[a] - lower[a];
+  }
+  const double tau_abs = mapped ? cfg.tau_abs / jacobian : cfg.tau_abs;
+
+  const RuleOrbits rule = build_rule_orbits(n);  // rule.cpp:166
+  const int d = cfg.init_subdiv > 0 ? cfg.init_subdiv : initial_subdivisions(n, cfg.init_target);
+  int64_t m = 1;  // geometry.cpp:86-94
+  for (int a = 0; a < n; ++a) {
+    if (m > cfg.max_regions / d) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
+    m *= d;
+  }
+  if (m > cfg.max_regions) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
+
+  ws.ensure(n, cfg.max_regions > m ? cfg.max_regions : m);
+  const int64_t cap = ws.cap;
+  const bool prof = cfg.profile != 0;
+  KTimer kt(ws, prof);
+
+  {  // uniform split of the unit cube
+    double lo[kMaxDim], step[kMaxDim];
+    for (int a = 0; a < n; ++a) {
+      lo[a] = 0.0;
+      step[a] = (1.0 - 0.0) / d;
+    }
+    PGN_CK(cudaMemcpyAsync(ws.d_lower.p, lo, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    PGN_CK(cudaMemcpyAsync(ws.d_step.p, step, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    const size_t a0 = kt.mark();
+    launch_uniform_split(st, n, d, m, cap, ws.low[0].p, ws.len[0].p, ws.d_lower.p, ws.d_step.p);
+    kt.span(PAGANI_K_INIT, a0, kt.mark());
+    out->kernel_launches[PAGANI_K_INIT]++;
+    out->h2d_bytes += 2 * n * sizeof(double);
+  }
+
+  EvalParams ep{};
+  ep.cap = cap;
+  ep.pest = ws.pest.p;
+  ep.est = ws.est.p;
+  ep.err = ws.err.p;
+  ep.axis = ws.axis.p;
+  ep.flag = ws.flag.p;
+  ep.rel_filter = cfg.rel_filtering_enabled ? 1 : 0;
+  ep.tau = cfg.tau_rel;
+  ep.n = n;
+  ep.mapped = mapped ? 1 : 0;
+  for (int k = 0; k < 5; ++k)
+    for (int o = 0; o < 5; ++o) ep.w[k][o] = rule.w[k][o];
+  for (int i = 0; i < 4; ++i) ep.gen[i] = rule.gen[i];
+  for (int a = 0; a < n; ++a) {
+    ep.map_lo[a] = lower[a];
+    ep.map_len[a] = dom_len[a];
+  }
+  ep.ip = di.params;
+  const uint64_t* g_exp = device_exp_table();
+  const double* g_sc = device_sincos_table();
+
+  Limits lim;
+  lim.direction_change_limit = cfg.direction_change_limit;
+  lim.attempt_limit = cfg.attempt_limit;
+  lim.p_max_start = cfg.p_max_start;
+  lim.p_max_step = cfg.p_max_step;
+  lim.p_max_cap = cfg.p_max_cap;
+
+  double acc_v = 0.0, acc_e = 0.0, acc_vf = 0.0, acc_ef = 0.0;  // Accumulators
+  double prev_total = std::numeric_limits<double>::quiet_NaN();
+  const int digits = convergence_digits(cfg.tau_rel);
+  out->regions_generated = m;
+  out->peak_regions = m;
+  int cur = 0;  // which low/len buffer holds the batch
+  double finished_volume = 0.0;
+
+  auto finish = [&](int status, int it) {
+    out->status = status;
+    out->iterations = it;
+    out->estimate = (acc_v + acc_vf) * jacobian;
+    out->errorest = (acc_e + acc_ef) * jacobian;
+  };
+
+  bool done = false;
+  for (int it = 1; it <= cfg.it_max && !done; ++it) {
+    // ---- evaluate (+ refine + classify) -------------------------------------
+    ep.m = m;
+    ep.low = ws.low[cur].p;
+    ep.len = ws.len[cur].p;
+    ep.refine = (it > 1 && cfg.refiner == PAGANI_REFINER_TWO_LEVEL) ? 1 : 0;
+    const size_t k0 = kt.mark();
+    eval_k<<<static_cast<unsigned>((m + kEvalThreads - 1) / kEvalThreads), kEvalThreads, 0, st>>>(
+        ep, g_exp, g_sc);
+    PGN_CK(cudaGetLastError());
+    const size_t k1 = kt.mark();
+    kt.span(PAGANI_K_EVALUATE, k0, k1);
+    out->kernel_launches[PAGANI_K_EVALUATE]++;
+    out->eval_count += m * rule.point_count;
+    out->region_evals += m;
+
+    // ---- block folds: v, e, finished sums, active counts ---------------------
+    const int64_t nblk = nblocks_of(m);
+    launch_fold_eval(st, m, ws.est.p, ws.err.p, ws.flag.p, ws.part_eval.p, ws.cnt_eval.p);
+    const size_t k2 = kt.mark();
+    launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
+                    ws.d_sc.p);
+    const size_t k3 = kt.mark();
+    kt.span(PAGANI_K_FOLD, k1, k2);
+    kt.span(PAGANI_K_FINALIZE, k2, k3);
+    out->kernel_launches[PAGANI_K_FOLD]++;
+    out->kernel_launches[PAGANI_K_FINALIZE]++;
+    PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
+    PGN_CK(cudaStreamSynchronize(st));
+    out->d2h_bytes += sizeof(FoldScalars);
+    const FoldScalars sc = ws.h_sc[0];
+    acc_v = sc.sum[0];  // block_sum(estimates)
+    acc_e = sc.sum[1];  // block_sum(errors)
+
+    pagani_trace_row row{};
+    row.it = it;
+    row.m = m;
+    row.active_rel = sc.count;
+
+    if (cfg.validate_invariants) {  // driver.cpp:75-79,148
+      launch_serial_volume(st, n, m, cap, ws.len[cur].p, nullptr, 0, ws.d_tmp.p);
+      double tv = 0;
+      PGN_CK(cudaMemcpyAsync(&tv, ws.d_tmp.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      PGN_CK(cudaStreamSynchronize(st));
+      if (std::fabs(tv + finished_volume - 1.0) > 1e-10)
+        throw std::logic_error("invariant violated: volume not conserved");
+    }
+
+    // check_termination (driver.cpp:43-46,150-152)
+    {
+      const double err_tot = acc_e + acc_ef;
+      if (err_tot <= std::fabs(acc_v + acc_vf) * cfg.tau_rel || err_tot <= tau_abs) {
+        row.v = acc_v, row.e = acc_e, row.v_f = acc_vf, row.e_f = acc_ef;
+        row.active_final = row.active_rel;
+        if (cfg.trace) cfg.trace(&row, cfg.trace_user);
+        finish(PAGANI_CONVERGED, it);
+        done = true;
+        break;
+      }
+    }
+    if (it == cfg.it_max) {
+      row.v = acc_v, row.e = acc_e, row.v_f = acc_vf, row.e_f = acc_ef;
+      row.active_final = row.active_rel;
+      if (cfg.trace) cfg.trace(&row, cfg.trace_user);
+      break;
+    }
+
+    // ---- triggers + threshold search (driver.cpp:154-172) --------------------
+    const int64_t active_count = sc.count;
+    const bool trig_memory = 2 * active_count > cfg.max_regions;
+    const bool trig_digits = digits_converged(prev_total, acc_v + acc_vf, digits);
+    row.trig_digits = trig_digits;
+    row.trig_memory = trig_memory;
+    bool use_t = false;
+    double t_accepted = 0.0;
+    double fin_v = sc.sum[2], fin_e = sc.sum[3];
+    int64_t kept = sc.count;
+    const int64_t* offsets = ws.off_eval.p;
+    if (trig_digits || trig_memory) {
+      double pms = 0.0;
+      const ThresholdOutcome tr =
+          device_threshold(ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf,
+                           acc_e + acc_ef, acc_e, m, cfg.tau_rel, lim, prof ? &pms : nullptr);
+      out->kernel_ms[PAGANI_K_PROBE] += pms;
+      out->kernel_launches[PAGANI_K_PROBE] += tr.attempts;
+      out->d2h_bytes += tr.attempts * sizeof(FoldScalars);
+      if (out->n_events < PAGANI_MAX_EVENTS) {
+        pagani_threshold_event& ev = out->events[out->n_events];
+        ev.iteration = it;
+        ev.success = tr.success;
+        ev.batch_size = m;
+        ev.finished_count = tr.finished_count;
+        ev.discarded_error = tr.discarded;
+        ev.budget_limit = tr.budget_limit;
+      }
+      out->n_events++;
+      const bool affordable = acc_ef + tr.discarded <= 0.25 * cfg.tau_rel * std::fabs(acc_v + acc_vf);
+      row.thr_invoked = 1;
+      row.thr_success = tr.success;
+      row.thr_attempts = tr.attempts;
+      row.thr_dir_changes = tr.direction_changes;
+      row.thr_threshold = tr.threshold;
+      row.thr_discarded = tr.discarded;
+      row.thr_budget = tr.budget_limit;
+      row.thr_finished = tr.finished_count;
+      if (tr.success && (trig_memory || affordable)) {
+        row.thr_accepted = 1;
+        use_t = true;
+        t_accepted = tr.threshold;
+        fin_e = tr.discarded;  // sum err[final flag == 0]
+        fin_v = tr.fin_v;
+        kept = m - tr.finished_count;
+        offsets = ws.off_probe.p;
+      }
+    }
+    row.v = acc_v, row.e = acc_e, row.v_f = acc_vf, row.e_f = acc_ef;
+    row.active_final = kept;
+    row.fin_v = fin_v;
+    row.fin_e = fin_e;
+    row.kept = kept;
+    if (cfg.trace) cfg.trace(&row, cfg.trace_user);
+
+    if (cfg.validate_invariants) {  // driver.cpp:185-198
+      const uint8_t* fflag = ws.flag.p;
+      if (use_t) {
+        launch_candidates(st, m, t_accepted, ws.flag.p, ws.err.p, ws.flag2.p);
+        fflag = ws.flag2.p;
+      }
+      launch_serial_volume(st, n, m, cap, ws.len[cur].p, fflag, 0, ws.d_tmp.p);
+      double fv = 0;
+      PGN_CK(cudaMemcpyAsync(&fv, ws.d_tmp.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      PGN_CK(cudaStreamSynchronize(st));
+      finished_volume += fv;
+      if (fin_e < 0.0) throw std::logic_error("invariant violated: negative finished error");
+    }
+
+    // ---- filter accounting (driver.cpp:194-202) -------------------------------
+    const double prev_e_f = acc_ef;
+    acc_vf += fin_v;
+    acc_ef += fin_e;
+    if (cfg.validate_invariants && acc_ef < prev_e_f)
+      throw std::logic_error("invariant violated: finished error decreased");
+    acc_v -= fin_v;
+    acc_e -= fin_e;
+    prev_total = acc_v + acc_vf;
+
+    if (kept == 0) {
+      finish(PAGANI_MAX_ITERATIONS, it);
+      done = true;
+      break;
+    }
+    if (2 * kept > cfg.max_regions) {
+      finish(PAGANI_MEMORY_EXHAUSTED, it);
+      done = true;
+      break;
+    }
+
+    // ---- fused filter + bisect into the other buffer ---------------------------
+    const size_t k4 = kt.mark();
+    launch_split(st, n, m, cap, cap, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p,
+                 ws.err.p, ws.axis.p, ws.low[cur].p, ws.len[cur].p, ws.low[cur ^ 1].p,
+                 ws.len[cur ^ 1].p, ws.pest.p, nullptr);
+    PGN_CK(cudaGetLastError());
+    kt.span(PAGANI_K_SPLIT, k4, kt.mark());
+    out->kernel_launches[PAGANI_K_SPLIT]++;
+    cur ^= 1;
+    m = 2 * kept;
+    out->regions_generated += m;
+    if (m > out->peak_regions) out->peak_regions = m;
+  }
+  if (!done) finish(PAGANI_MAX_ITERATIONS, cfg.it_max);
+  PGN_CK(cudaStreamSynchronize(st));
+  kt.collect(out);
+  out->wall_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();
+}
+
+}  // namespace pgn

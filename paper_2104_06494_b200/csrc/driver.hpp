@@ -1,0 +1,115 @@
+// Host-side PAGANI driver (C++): the reference's integrate() loop
+// (/root/reference/proj/src/driver.cpp:83-215) over device-resident batches.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pagani.h"
+#include "kernels.cuh"
+#include "rule.hpp"
+
+namespace pgn {
+
+struct CudaError : std::runtime_error {
+  explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+struct UnsupportedError : std::runtime_error {
+  explicit UnsupportedError(const std::string& s) : std::runtime_error(s) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define PGN_CK(x) ::pgn::cuda_check((x), #x)
+
+// Device buffer with RAII (batch API temporaries).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    free();
+    n = count;
+    if (count) PGN_CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { free(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// Per-device cached workspace: the region store (double-buffered, axis-major)
+// and the scratch of the folds.  Sized once for `cap` regions of dimension
+// n and reused by every later call with cap' <= cap.
+struct Workspace {
+  int device = -1;
+  cudaStream_t st = nullptr;
+  std::mutex mu;
+  int n = 0;
+  int64_t cap = 0;
+  int64_t nblk_cap = 0;
+  DevBuf<double> low[2], len[2];
+  DevBuf<double> pest, est, err;
+  DevBuf<uint8_t> axis, flag, flag2;
+  DevBuf<double> part_eval, part_probe, scratch;
+  DevBuf<int64_t> cnt_eval, cnt_probe, off_eval, off_probe;
+  DevBuf<FoldScalars> d_sc;
+  DevBuf<unsigned long long> mm_keys;
+  DevBuf<double> mm_out, d_lower, d_step, d_tmp;
+  FoldScalars* h_sc = nullptr;  // pinned [2]
+  double* h_mm = nullptr;       // pinned [4]
+  std::vector<cudaEvent_t> ev;
+  void ensure(int n, int64_t cap);
+  cudaEvent_t event(size_t i);
+  ~Workspace();
+};
+
+Workspace& workspace_for(int device);
+void release_workspaces();
+
+// Integrand descriptor resolved to a device kernel.
+struct DeviceIntegrand {
+  int fid = 0;
+  IntegrandParams params{};
+};
+DeviceIntegrand resolve_integrand(const pagani_integrand* f);
+
+struct ThresholdOutcome {
+  bool success = false;
+  double threshold = 0.0, discarded = 0.0, budget_limit = 0.0;
+  int64_t finished_count = 0;
+  int attempts = 0, direction_changes = 0;
+  double fin_v = 0.0;  // sum of estimates where candidate == 0 (valid on success)
+};
+
+struct Limits {
+  int direction_change_limit = 4, attempt_limit = 40;
+  double p_max_start = 0.25, p_max_step = 0.10, p_max_cap = 0.95;
+};
+
+// classify.cpp:37-95 over device arrays (flags unchanged; candidates are
+// re-derived from the returned threshold).  Leaves, on success, the probe's
+// block offsets in ws.off_probe.
+ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
+                                  const double* d_err, const uint8_t* d_flag, double v_tot,
+                                  double e_tot, double e_it, int64_t s_it, double tau_rel,
+                                  const Limits& lim, double* probe_ms);
+
+void integrate(const pagani_integrand* f, int ndim, const double* lower, const double* upper,
+               const pagani_config* cfg, pagani_result* out);
+
+bool digits_converged(double v_prev, double v_curr, int digits);
+int convergence_digits(double tau_rel);
+int initial_subdivisions(int n, int64_t init_target);
+
+}  // namespace pgn

@@ -1,0 +1,34 @@
+// k_evaluate instantiations for the reference integrand f5, n = 1..16,
+// parity and fast modes (one TU per integrand so nvcc builds them in parallel).
+#include "kernels.cuh"
+
+namespace pgn {
+
+template <int N>
+static EvalKernel pick_f5(int mode) {
+  return mode ? &k_evaluate_sep<N, F5, 1> : &k_evaluate_sep<N, F5, 0>;
+}
+
+EvalKernel lookup_eval_f5(int n, int mode) {
+  switch (n) {
+    case 1: return pick_f5<1>(mode);
+    case 2: return pick_f5<2>(mode);
+    case 3: return pick_f5<3>(mode);
+    case 4: return pick_f5<4>(mode);
+    case 5: return pick_f5<5>(mode);
+    case 6: return pick_f5<6>(mode);
+    case 7: return pick_f5<7>(mode);
+    case 8: return pick_f5<8>(mode);
+    case 9: return pick_f5<9>(mode);
+    case 10: return pick_f5<10>(mode);
+    case 11: return pick_f5<11>(mode);
+    case 12: return pick_f5<12>(mode);
+    case 13: return pick_f5<13>(mode);
+    case 14: return pick_f5<14>(mode);
+    case 15: return pick_f5<15>(mode);
+    case 16: return pick_f5<16>(mode);
+    default: return nullptr;
+  }
+}
+
+}  // namespace pgn

@@ -1,0 +1,214 @@
+// glibc 2.39 `exp` and `cos`, restated for host and device, bit-for-bit.
+//
+// Why: the reference evaluates its integrands with the platform libm
+// (`/root/reference/proj/src/integrands.cpp:27,51,57,66`).  On an FMA-capable
+// x86-64 host glibc's IFUNCs select `__exp_fma` / `__cos_fma`, i.e. the C
+// sources of sysdeps/ieee754/dbl-64/e_exp.c (ARM optimized-routines exp,
+// N = 128 table) and s_sin.c (IBM Accurate Mathematical Library cos) compiled
+// with -mfma, where GCC contracted some products into FMAs.  CUDA's libdevice
+// exp/cos are different algorithms and differ in the last ulp on ~1e-3 of
+// arguments.  This header restates those two routines with the
+// SAME operation order and the SAME fused/unfused choices as the shipped
+// machine code (read from `objdump -d libm.so.6`), and
+// the same tables (glibc_tables.h, extracted by tools/extract_glibc_tables.py).
+// Bit-equality with the host libm is checked by tests/test_glibc_math.py on
+// the CPU and tests/test_gpu_parity.py on the B200.
+//
+// Every arithmetic op goes through fp_ops.cuh so nvcc cannot contract it.
+// Round-to-nearest is assumed (glibc switches to it when needed; CUDA always
+// rounds to nearest).
+#pragma once
+
+#include "fp_ops.cuh"
+#include "glibc_tables.h"
+
+namespace pgn {
+
+// ---- exp: sysdeps/ieee754/dbl-64/e_exp.c (glibc 2.39), __exp_fma ---------
+namespace expc {
+constexpr uint64_t kInvLn2N = 0x40671547652b82feULL;   // 0x1.71547652b82fep7
+constexpr uint64_t kShift = 0x4338000000000000ULL;     // 0x1.8p52
+constexpr uint64_t kNegLn2hiN = 0xbf762e42fefa0000ULL; // -0x1.62e42fefa0000p-8
+constexpr uint64_t kNegLn2loN = 0xbd0cf79abc9e3b3aULL; // -0x1.cf79abc9e3b3ap-47
+constexpr uint64_t kC2 = 0x3fdffffffffffdbdULL;
+constexpr uint64_t kC3 = 0x3fc555555555543cULL;
+constexpr uint64_t kC4 = 0x3fa55555cf172b91ULL;
+constexpr uint64_t kC5 = 0x3f81111167a4d017ULL;
+}  // namespace expc
+
+// e_exp.c specialcase(): result near the overflow/underflow boundaries.
+PGN_HD double gm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+  if ((ki & 0x80000000ULL) == 0) {
+    // k > 0: the exponent of scale may have overflowed by <= 460.
+    sbits -= 1009ULL << 52;
+    const double scale = pgn_asf64(sbits);
+    return P_MUL(P_FMA(scale, tmp, scale), 0x1p1009);
+  }
+  // k < 0: careful rounding in the subnormal range (unfused in __exp_fma:
+  // the product scale*tmp is reused for `lo`).
+  sbits += 1022ULL << 52;
+  const double scale = pgn_asf64(sbits);
+  const double st = P_MUL(scale, tmp);
+  double y = P_ADD(scale, st);
+  if (y < 1.0) {
+    double lo = P_ADD(P_SUB(scale, y), st);
+    const double hi = P_ADD(1.0, y);
+    lo = P_ADD(P_ADD(P_SUB(1.0, hi), y), lo);
+    y = P_SUB(P_ADD(hi, lo), 1.0);
+    if (y == 0.0) y = 0.0;  // avoid -0.0
+  }
+  return P_MUL(0x1p-1022, y);
+}
+
+PGN_HD double gm_exp(double x, const uint64_t* __restrict__ T) {
+  using namespace expc;
+  const uint64_t ix = pgn_asu64(x);
+  uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ff;
+  if (abstop - 0x3c9u >= 0x3fu) {
+    if (static_cast<int32_t>(abstop - 0x3c9u) < 0) return P_ADD(1.0, x);  // |x| < 2^-54
+    if (abstop >= 0x409u) {                                               // |x| >= 1024
+      if (ix == 0xfff0000000000000ULL) return 0.0;
+      if (abstop >= 0x7ffu) return P_ADD(1.0, x);
+      if (ix >> 63) return 0.0;                          // __math_uflow(0)
+      return pgn_asf64(0x7ff0000000000000ULL);           // __math_oflow(0)
+    }
+    abstop = 0;  // large |x|: handled by the special case below
+  }
+  double kd = P_FMA(x, pgn_asf64(kInvLn2N), pgn_asf64(kShift));
+  const uint64_t ki = pgn_asu64(kd);
+  kd = P_SUB(kd, pgn_asf64(kShift));
+  double r = P_FMA(kd, pgn_asf64(kNegLn2hiN), x);
+  r = P_FMA(kd, pgn_asf64(kNegLn2loN), r);
+  const uint64_t idx = 2 * (ki & 127);
+  const uint64_t top = ki << 45;
+  const double tail = pgn_asf64(T[idx]);
+  const uint64_t sbits = T[idx + 1] + top;
+  const double p23 = P_FMA(r, pgn_asf64(kC3), pgn_asf64(kC2));
+  const double tr = P_ADD(r, tail);
+  const double r2 = P_MUL(r, r);
+  const double p45 = P_FMA(r, pgn_asf64(kC5), pgn_asf64(kC4));
+  const double t = P_FMA(p23, r2, tr);
+  const double r4 = P_MUL(r2, r2);
+  const double tmp = P_FMA(r4, p45, t);
+  if (abstop == 0) return gm_exp_special(tmp, sbits, ki);
+  const double scale = pgn_asf64(sbits);
+  return P_FMA(scale, tmp, scale);
+}
+
+// ---- cos: sysdeps/ieee754/dbl-64/s_sin.c (glibc 2.39), __cos_fma ---------
+namespace cosc {
+constexpr uint64_t kBig = 0x42c8000000000000ULL;    // 0x1.8p45
+constexpr uint64_t kSn3 = 0xbfc5555555555515ULL;
+constexpr uint64_t kSn5 = 0x3f811110e829872fULL;
+constexpr uint64_t kCs2 = 0x3fe0000000000000ULL;
+constexpr uint64_t kCs4 = 0xbfa5555555555535ULL;
+constexpr uint64_t kCs6 = 0x3f56c16bedd9e239ULL;
+constexpr uint64_t kS1 = 0xbfc5555555555555ULL;
+constexpr uint64_t kS2 = 0x3f81111111110eceULL;
+constexpr uint64_t kS3 = 0xbf2a01a019db08b8ULL;
+constexpr uint64_t kS4 = 0x3ec71de27b9a7ed9ULL;
+constexpr uint64_t kS5 = 0xbe5addffc2fcdf59ULL;
+constexpr uint64_t kHp0 = 0x3ff921fb54442d18ULL;
+constexpr uint64_t kHp1 = 0x3c91a62633145c07ULL;
+constexpr uint64_t kToint = 0x4338000000000000ULL;
+constexpr uint64_t kHpinv = 0x3fe45f306dc9c883ULL;
+constexpr uint64_t kMp1 = 0x3ff921fb58000000ULL;
+constexpr uint64_t kMp2 = 0xbe4dde973c000000ULL;
+constexpr uint64_t kPp3 = 0xbc8cb3b398000000ULL;
+constexpr uint64_t kPp4 = 0xbacd747f23e32ed7ULL;
+constexpr uint64_t kTaylorMax = 0x3fc020c49ba5e354ULL;  // 0.126
+}  // namespace cosc
+
+#define PGN_C(name) pgn_asf64(cosc::name)
+
+// s_sin.c do_cos(x, dx)
+PGN_HD double gm_do_cos(double x, double dx, const double* __restrict__ SC) {
+  if (x < 0) dx = -dx;
+  const double ax = pgn_fabs(x);
+  const double u = P_ADD(PGN_C(kBig), ax);
+  const double xr = P_ADD(P_SUB(ax, P_SUB(u, PGN_C(kBig))), dx);
+  const double xx = P_MUL(xr, xr);
+  const double s = P_FMA(P_MUL(xr, xx), P_FMA(xx, PGN_C(kSn5), PGN_C(kSn3)), xr);
+  const double c =
+      P_MUL(xx, P_FMA(xx, P_FMA(xx, PGN_C(kCs6), PGN_C(kCs4)), PGN_C(kCs2)));
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  const double sn = SC[k], ssn = SC[k + 1], cs = SC[k + 2], ccs = SC[k + 3];
+  double cor = P_FMA(-s, ssn, ccs);
+  cor = P_FMA(-c, cs, cor);
+  cor = P_FMA(-s, sn, cor);
+  return P_ADD(cs, cor);
+}
+
+// s_sin.c do_sin(x, dx), including the TAYLOR_SIN branch.
+PGN_HD double gm_do_sin(double x, double dx, const double* __restrict__ SC) {
+  if (pgn_fabs(x) < PGN_C(kTaylorMax)) {
+    const double xx = P_MUL(x, x);
+    double p = P_FMA(PGN_C(kS5), xx, PGN_C(kS4));
+    p = P_FMA(p, xx, PGN_C(kS3));
+    p = P_FMA(p, xx, PGN_C(kS2));
+    p = P_FMA(p, xx, PGN_C(kS1));
+    const double t = P_FMA(xx, P_FMA(p, x, -P_MUL(0.5, dx)), dx);
+    return P_ADD(x, t);
+  }
+  const double xold = x;
+  if (x <= 0) dx = -dx;
+  const double ax = pgn_fabs(x);
+  const double u = P_ADD(PGN_C(kBig), ax);
+  const double xr = P_SUB(ax, P_SUB(u, PGN_C(kBig)));
+  const double xx = P_MUL(xr, xr);
+  const double s = P_ADD(xr, P_FMA(P_MUL(xr, xx), P_FMA(xx, PGN_C(kSn5), PGN_C(kSn3)), dx));
+  const double c = P_FMA(
+      xr, dx, P_MUL(xx, P_FMA(xx, P_FMA(xx, PGN_C(kCs6), PGN_C(kCs4)), PGN_C(kCs2))));
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  const double sn = SC[k], ssn = SC[k + 1], cs = SC[k + 2], ccs = SC[k + 3];
+  double cor = P_FMA(s, ccs, ssn);
+  cor = P_FMA(-c, sn, cor);
+  cor = P_FMA(s, cs, cor);
+  const double r = P_ADD(sn, cor);
+  return pgn_asf64((pgn_asu64(r) & 0x7fffffffffffffffULL) |
+                   (pgn_asu64(xold) & 0x8000000000000000ULL));
+}
+
+// Returns false when |x| >= 105414350 (glibc's __branred range), which the
+// restatement does not cover; callers fall back and lose bit-equality there.
+PGN_HD bool gm_cos_in_range(double x) {
+  const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
+  return k < 0x419921fbu;
+}
+
+PGN_HD double gm_cos(double x, const double* __restrict__ SC) {
+  const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
+  if (k < 0x3e400000u) return 1.0;          // |x| < 2^-27
+  if (k < 0x3feb6000u) return gm_do_cos(x, 0.0, SC);  // |x| < 0.855469
+  if (k < 0x400368fdu) {                     // |x| < 2.426265
+    const double y = P_SUB(PGN_C(kHp0), pgn_fabs(x));
+    const double a = P_ADD(y, PGN_C(kHp1));
+    const double da = P_ADD(P_SUB(y, a), PGN_C(kHp1));
+    return gm_do_sin(a, da, SC);
+  }
+  if (k < 0x419921fbu) {                     // |x| < 105414350: reduce_sincos
+    const double t = P_FMA(x, PGN_C(kHpinv), PGN_C(kToint));
+    const double xn = P_SUB(t, PGN_C(kToint));
+    const int n = static_cast<int>(pgn_asu64(t) & 3);
+    const double y = P_FMA(-xn, PGN_C(kMp2), P_FMA(-xn, PGN_C(kMp1), x));
+    const double t2 = P_FMA(-xn, PGN_C(kPp3), y);
+    double db = P_FMA(-xn, PGN_C(kPp3), P_SUB(y, t2));
+    const double b = P_FMA(-xn, PGN_C(kPp4), t2);
+    db = P_ADD(db, P_FMA(-xn, PGN_C(kPp4), P_SUB(t2, b)));
+    const double r = (n & 1) ? gm_do_sin(b, db, SC) : gm_do_cos(b, db, SC);
+    return ((n + 1) & 2) ? -r : r;
+  }
+  if (k < 0x7ff00000u) {
+    // __branred territory (|x| >= 105414350): not restated.
+#if defined(__CUDA_ARCH__)
+    return ::cos(x);
+#else
+    return std::cos(x);
+#endif
+  }
+  return P_DIV(x, x);  // inf or nan -> nan
+}
+
+#undef PGN_C
+
+}  // namespace pgn

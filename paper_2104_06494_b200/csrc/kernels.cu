@@ -1,0 +1,558 @@
+// Region-store kernels (see kernels.cuh).  All are HBM/latency bound; the
+// data layout is axis-major SoA (low[a*cap + j]) so every per-region access
+// is coalesced across the warp, and children of kept region k are written
+// as 16-byte pairs (2k, 2k+1).
+#include "kernels.cuh"
+
+#include "glibc_tables.h"
+
+namespace pgn {
+
+namespace {
+
+__device__ const uint64_t g_exp_tab[256] = PGN_EXP_TAB_INIT;
+__device__ const uint64_t g_sincos_tab[440] = PGN_SINCOS_TAB_INIT;
+
+inline unsigned grid_for(int64_t work, int threads) {
+  return static_cast<unsigned>((work + threads - 1) / threads);
+}
+
+// ---- uniform split ----------------------------------------------------------
+__global__ void k_uniform_split(int n, int d, int64_t m, int64_t cap, double* low, double* len,
+                                const double* lower, const double* step) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  int64_t rem = j;
+  for (int a = 0; a < n; ++a) {  // geometry.cpp:100-110, axis 0 fastest
+    const int64_t cell = rem % d;
+    rem /= d;
+    low[a * cap + j] = P_ADD(lower[a], P_MUL(static_cast<double>(cell), step[a]));
+    len[a * cap + j] = step[a];
+  }
+}
+
+// ---- deterministic block folds ----------------------------------------------
+// One thread per (block, quantity): the serial left fold over <= 2048 values
+// (reduce.cpp:36-43 / 54-62).  The fold is a dependent DADD chain, so the
+// loads are batched 8 ahead.  Masked folds add +0.0 for skipped entries,
+// which equals skipping: the running sum starts at +0.0 and can never become
+// -0.0 under round-to-nearest.
+template <bool MASKED>
+__device__ __forceinline__ double serial_fold(const double* __restrict__ x,
+                                              const uint8_t* __restrict__ f, uint8_t which,
+                                              int64_t lo, int64_t hi, int64_t* cnt_other) {
+  double s = 0.0;
+  int64_t c = 0;
+  int64_t i = lo;
+  for (; i + 8 <= hi; i += 8) {
+    double v[8];
+    uint8_t g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      v[u] = __ldg(x + i + u);
+      if (MASKED) g[u] = __ldg(f + i + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (MASKED) {
+        const bool take = g[u] == which;
+        c += take ? 0 : 1;
+        s = P_ADD(s, take ? v[u] : 0.0);
+      } else {
+        s = P_ADD(s, v[u]);
+      }
+    }
+  }
+  for (; i < hi; ++i) {
+    const double v = __ldg(x + i);
+    if (MASKED) {
+      const bool take = __ldg(f + i) == which;
+      c += take ? 0 : 1;
+      s = P_ADD(s, take ? v : 0.0);
+    } else {
+      s = P_ADD(s, v);
+    }
+  }
+  if (cnt_other) *cnt_other = c;
+  return s;
+}
+
+__global__ void k_fold_eval(int64_t m, int64_t nblk, const double* __restrict__ est,
+                            const double* __restrict__ err, const uint8_t* __restrict__ flag,
+                            double* part, int64_t* cnt) {
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t b = gid >> 2;
+  const int q = static_cast<int>(gid & 3);
+  if (b >= nblk) return;
+  const int64_t lo = b * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
+  const double* x = (q & 1) ? err : est;
+  double s;
+  if (q < 2) {
+    s = serial_fold<false>(x, nullptr, 0, lo, hi, nullptr);
+  } else {
+    int64_t active = 0;  // entries with flag != 0
+    s = serial_fold<true>(x, flag, 0, lo, hi, &active);
+    if (q == 2) cnt[b] = active;
+  }
+  part[q * nblk + b] = s;
+}
+
+__global__ void k_probe(int64_t m, int64_t nblk, double t, const double* __restrict__ est,
+                        const double* __restrict__ err, const uint8_t* __restrict__ flag,
+                        double* part, int64_t* cnt) {
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t b = gid >> 2;
+  const int q = static_cast<int>(gid & 3);
+  if (b >= nblk || q == 3) return;
+  const int64_t lo = b * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
+  // candidate = active & !(err < t)   (classify.cpp:29-35, 63-66)
+  // q0: sum err where candidate == 0  (classify.cpp:70)
+  // q1: sum est where candidate == 0  (classify.cpp:104, used if accepted)
+  // q2: count candidate == 1          (classify.cpp:68)
+  const double* x = q == 1 ? est : err;
+  double s = 0.0;
+  int64_t c = 0;
+  int64_t i = lo;
+  for (; i + 8 <= hi; i += 8) {
+    double v[8], e[8];
+    uint8_t g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      e[u] = __ldg(err + i + u);
+      v[u] = q == 1 ? __ldg(x + i + u) : e[u];
+      g[u] = __ldg(flag + i + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool c1 = g[u] && !(e[u] < t);
+      c += c1;
+      if (q < 2) s = P_ADD(s, c1 ? 0.0 : v[u]);
+    }
+  }
+  for (; i < hi; ++i) {
+    const double e = __ldg(err + i);
+    const bool c1 = __ldg(flag + i) && !(e < t);
+    c += c1;
+    if (q < 2) s = P_ADD(s, c1 ? 0.0 : (q == 1 ? __ldg(est + i) : e));
+  }
+  if (q < 2)
+    part[q * nblk + b] = s;
+  else
+    cnt[b] = c;
+}
+
+__global__ void k_candidates(int64_t m, double t, const uint8_t* flag, const double* err,
+                             uint8_t* out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < m) out[j] = (flag[j] && !(err[j] < t)) ? 1 : 0;
+}
+
+__global__ void k_fold_one(int64_t m, int64_t nblk, const double* __restrict__ x,
+                           const uint8_t* __restrict__ flag, int which, double* part,
+                           int64_t* cnt) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  const int64_t lo = b * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
+  int64_t other = 0;
+  const double s = flag ? serial_fold<true>(x, flag, static_cast<uint8_t>(which), lo, hi, &other)
+                        : serial_fold<false>(x, nullptr, 0, lo, hi, nullptr);
+  part[b] = s;
+  if (cnt) cnt[b] = (hi - lo) - other;  // entries equal to `which`
+}
+
+// ---- pairwise tree + offsets (single CTA) -----------------------------------
+constexpr int kFinThreads = 1024;
+
+__global__ void __launch_bounds__(kFinThreads)
+    k_finalize(int64_t nblk, int nq, const double* part, const int64_t* cnt, int64_t* offsets,
+               double* scratch, FoldScalars* out) {
+  __shared__ int64_t s_sum[kFinThreads];
+  const int tid = threadIdx.x;
+  // reduce.cpp:13-27: p[i] = p[2i] + p[2i+1] level by level, odd tail carried.
+  for (int q = 0; q < nq; ++q) {
+    const double* src = part + q * nblk;
+    double* bufs[2] = {scratch, scratch + nblk};
+    int cur_buf = 0;
+    int64_t cur = nblk;
+    while (cur > 1) {
+      const int64_t half = cur / 2;
+      double* dst = bufs[cur_buf];
+      for (int64_t i = tid; i < half; i += kFinThreads) dst[i] = P_ADD(src[2 * i], src[2 * i + 1]);
+      if ((cur & 1) && tid == 0) dst[half] = src[cur - 1];
+      __syncthreads();
+      src = dst;
+      cur_buf ^= 1;
+      cur = half + (cur & 1);
+    }
+    if (tid == 0) out->sum[q] = nblk ? src[0] : 0.0;
+    __syncthreads();
+  }
+  if (!cnt) {
+    if (tid == 0) out->count = 0;
+    return;
+  }
+  // exclusive scan of per-block counts (exact integers)
+  const int64_t chunk = (nblk + kFinThreads - 1) / kFinThreads;
+  const int64_t lo = tid * chunk, hi = lo + chunk < nblk ? lo + chunk : nblk;
+  int64_t local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += cnt[i];
+  s_sum[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < kFinThreads; off <<= 1) {
+    const int64_t v = tid >= off ? s_sum[tid - off] : 0;
+    __syncthreads();
+    s_sum[tid] += v;
+    __syncthreads();
+  }
+  int64_t run = s_sum[tid] - local;
+  if (offsets)
+    for (int64_t i = lo; i < hi; ++i) {
+      offsets[i] = run;
+      run += cnt[i];
+    }
+  if (tid == kFinThreads - 1) out->count = s_sum[tid];
+}
+
+// ---- min / max ---------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+  const unsigned long long b = pgn_asu64(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double key_val(unsigned long long k) {
+  return pgn_asf64((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k);
+}
+
+__global__ void k_minmax_init(unsigned long long* keys) {
+  keys[0] = ~0ULL;
+  keys[1] = 0ULL;
+}
+
+__global__ void k_minmax(int64_t m, const double* __restrict__ x, unsigned long long* keys) {
+  unsigned long long lo = ~0ULL, hi = 0ULL;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = __ldg(x + i);
+    if (v != v) continue;  // NaN never wins a comparison (reduce.cpp:77-78)
+    const unsigned long long k = ord_key(v);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = h2 > hi ? h2 : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(keys, lo);
+    atomicMax(keys + 1, hi);
+  }
+}
+
+__global__ void k_minmax_done(int64_t m, const double* x, const unsigned long long* keys,
+                              double* out) {
+  // reduce.cpp:75-76: both start at x[0]; a NaN there sticks.
+  const double x0 = m ? x[0] : 0.0;
+  if (m == 0 || x0 != x0) {
+    out[0] = x0;
+    out[1] = x0;
+    return;
+  }
+  out[0] = key_val(keys[0]);
+  out[1] = key_val(keys[1]);
+}
+
+// ---- fused filter + bisect ---------------------------------------------------
+constexpr int kSplitThreads = 256;
+constexpr int kSplitPer = static_cast<int>(kBlock) / kSplitThreads;  // 8
+
+// Rank of each kept region inside its 2048-block: warp ballots + CTA scan.
+__device__ __forceinline__ int64_t cta_rank(bool keep, int r, int64_t& carry, int* s_warp) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  const int before = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) s_warp[wid] = __popc(bal);
+  __syncthreads();
+  int wbase = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kSplitThreads / 32; ++w) {
+    const int c = s_warp[w];
+    wbase += w < wid ? c : 0;
+    total += c;
+  }
+  __syncthreads();
+  const int64_t rank = carry + wbase + before;
+  carry += total;
+  (void)r;
+  return rank;
+}
+
+__global__ void __launch_bounds__(kSplitThreads)
+    k_split(int n, int64_t m, int64_t cap_src, int64_t cap_dst, const uint8_t* __restrict__ flag,
+            int use_t, double t, const int64_t* __restrict__ offsets, const double* __restrict__ est,
+            const double* __restrict__ err, const uint8_t* __restrict__ axis,
+            const double* __restrict__ low, const double* __restrict__ len, double* dlow,
+            double* dlen, double* dpest, double* dperr) {
+  __shared__ int s_warp[kSplitThreads / 32];
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlock;
+  int64_t carry = offsets ? offsets[b] : base;
+  for (int r = 0; r < kSplitPer; ++r) {
+    const int64_t j = base + r * kSplitThreads + threadIdx.x;
+    bool keep = j < m && (flag ? __ldg(flag + j) != 0 : true);
+    if (use_t && keep) keep = !(__ldg(err + j) < t);  // accepted threshold (classify.cpp:63-66)
+    const int64_t k = cta_rank(keep, r, carry, s_warp);
+    if (!keep) continue;
+    const int ax = __ldg(axis + j);
+    const int64_t c0 = 2 * k;
+    for (int a = 0; a < n; ++a) {  // geometry.cpp:122-141
+      const double lo = __ldg(low + a * cap_src + j);
+      const double ln = __ldg(len + a * cap_src + j);
+      double2 cl, cn;
+      if (a == ax) {
+        const double half = P_MUL(ln, 0.5);
+        cl = make_double2(lo, P_ADD(lo, half));
+        cn = make_double2(half, half);
+      } else {
+        cl = make_double2(lo, lo);
+        cn = make_double2(ln, ln);
+      }
+      *reinterpret_cast<double2*>(dlow + a * cap_dst + c0) = cl;
+      *reinterpret_cast<double2*>(dlen + a * cap_dst + c0) = cn;
+    }
+    const double e = __ldg(est + j);
+    *reinterpret_cast<double2*>(dpest + c0) = make_double2(e, e);
+    if (dperr) {
+      const double r2 = __ldg(err + j);
+      *reinterpret_cast<double2*>(dperr + c0) = make_double2(r2, r2);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSplitThreads)
+    k_compact(int n, int64_t m, int64_t cap, const uint8_t* __restrict__ flag,
+              const int64_t* __restrict__ offsets, const double* low, const double* len,
+              const double* est, const double* err, const int32_t* axis, const double* pest,
+              const double* perr, double* klow, double* klen, double* kest, double* kerr,
+              int32_t* kaxis, double* kpest, double* kperr) {
+  __shared__ int s_warp[kSplitThreads / 32];
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlock;
+  int64_t carry = offsets[b];
+  for (int r = 0; r < kSplitPer; ++r) {
+    const int64_t j = base + r * kSplitThreads + threadIdx.x;
+    const bool keep = j < m && flag[j] != 0;
+    const int64_t k = cta_rank(keep, r, carry, s_warp);
+    if (!keep) continue;
+    for (int a = 0; a < n; ++a) {
+      klow[a * cap + k] = low[a * cap + j];
+      klen[a * cap + k] = len[a * cap + j];
+    }
+    kest[k] = est[j];
+    kerr[k] = err[j];
+    kaxis[k] = axis[j];
+    kpest[k] = pest[j];
+    kperr[k] = perr[j];
+  }
+}
+
+// ---- batch-API elementwise kernels -------------------------------------------
+__global__ void k_refine(int64_t m, const double* est, const double* raw, const double* pest,
+                         double* out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int64_t s = j ^ 1;  // errorest.cpp:24-36
+  const double pair = P_ADD(raw[j], raw[s]);
+  if (pair == 0.0 || !pgn_isfinite(pair)) {
+    out[j] = raw[j];
+    return;
+  }
+  const double delta = pgn_fabs(P_SUB(pest[j], P_ADD(est[j], est[s])));
+  const double r = P_DIV(delta, pair);
+  const double scale = r < 0.125 ? 0.125 : (1.0 < r ? 1.0 : r);
+  out[j] = P_MUL(raw[j], scale);
+}
+
+__global__ void k_classify(int64_t m, const double* est, const double* err, double tau,
+                           int enabled, uint8_t* flags) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  if (!enabled) {
+    flags[j] = 1;
+    return;
+  }
+  const bool fin = est[j] == 0.0 ? err[j] == 0.0 : err[j] <= P_MUL(pgn_fabs(est[j]), tau);
+  flags[j] = fin ? 0 : 1;
+}
+
+__global__ void k_apply_threshold(int64_t m, const double* err, double t, uint8_t* flags) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < m) flags[j] = err[j] < t ? 0 : 1;  // classify.cpp:29-35
+}
+
+// Naive serial volume sum (geometry.cpp:48-52 / classify.cpp:128-131), for
+// the validation-only quantities.  One thread: it must be serial to match.
+__global__ void k_serial_volume(int n, int64_t m, int64_t cap, const double* len,
+                                const uint8_t* flag, int which, double* out) {
+  double s = 0.0;
+  for (int64_t j = 0; j < m; ++j) {
+    if (flag && flag[j] != which) continue;
+    double v = 1.0;
+    for (int a = 0; a < n; ++a) v = P_MUL(v, len[a * cap + j]);
+    s = P_ADD(s, v);
+  }
+  *out = s;
+}
+
+__global__ void k_math(int which, int64_t m, const double* x, double* y) {
+  __shared__ uint64_t s_exp[256];
+  __shared__ double s_sc[440];
+  load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  y[j] = which == 0 ? gm_exp(x[j], s_exp) : gm_cos(x[j], s_sc);
+}
+
+template <class F>
+__global__ void k_call(int n, int64_t m, const double* x, IntegrandParams ip, double* y) {
+  __shared__ uint64_t s_exp[256];
+  __shared__ double s_sc[440];
+  load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const MathTables T{s_exp, s_sc};
+  double xx[16];
+  for (int a = 0; a < n; ++a) xx[a] = x[j * n + a];
+  y[j] = eval_point<F>(xx, n, ip, T);
+}
+
+}  // namespace
+
+const uint64_t* device_exp_table() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_exp_tab);
+  return static_cast<const uint64_t*>(p);
+}
+const double* device_sincos_table() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_sincos_tab);
+  return static_cast<const double*>(p);
+}
+
+void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap, double* low,
+                          double* len, const double* lower, const double* step) {
+  if (m <= 0) return;
+  k_uniform_split<<<grid_for(m, 256), 256, 0, st>>>(n, d, m, cap, low, len, lower, step);
+}
+
+void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
+                      const uint8_t* flag, double* part, int64_t* cnt) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_fold_eval<<<grid_for(nblk * 4, 128), 128, 0, st>>>(m, nblk, est, err, flag, part, cnt);
+}
+
+void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const double* err,
+                  const uint8_t* flag, double* part, int64_t* cnt) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_probe<<<grid_for(nblk * 4, 128), 128, 0, st>>>(m, nblk, t, est, err, flag, part, cnt);
+}
+
+void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,
+                       const double* err, uint8_t* out) {
+  if (m > 0) k_candidates<<<grid_for(m, 256), 256, 0, st>>>(m, t, flag, err, out);
+}
+
+void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t* flag,
+                     int which, double* part, int64_t* cnt) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_fold_one<<<grid_for(nblk, 128), 128, 0, st>>>(m, nblk, x, flag, which, part, cnt);
+}
+
+void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
+                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out) {
+  k_finalize<<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out);
+}
+
+void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,
+                   double* out) {
+  k_minmax_init<<<1, 1, 0, st>>>(keys);
+  if (m > 0) {
+    int blocks = static_cast<int>(grid_for(m, 256));
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_minmax<<<blocks, 256, 0, st>>>(m, x, keys);
+  }
+  k_minmax_done<<<1, 1, 0, st>>>(m, x, keys, out);
+}
+
+void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
+                  const uint8_t* flag, int use_t, double t, const int64_t* offsets,
+                  const double* est,
+                  const double* err, const uint8_t* axis, const double* low, const double* len,
+                  double* dlow, double* dlen, double* dpest, double* dperr) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_split<<<static_cast<unsigned>(nblk), kSplitThreads, 0, st>>>(
+      n, m, cap_src, cap_dst, flag, use_t, t, offsets, est, err, axis, low, len, dlow, dlen,
+      dpest, dperr);
+}
+
+void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
+                    const int64_t* offsets, const double* low, const double* len,
+                    const double* est, const double* err, const int32_t* axis,
+                    const double* pest, const double* perr, double* klow, double* klen,
+                    double* kest, double* kerr, int32_t* kaxis, double* kpest, double* kperr) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_compact<<<static_cast<unsigned>(nblk), kSplitThreads, 0, st>>>(
+      n, m, cap, flag, offsets, low, len, est, err, axis, pest, perr, klow, klen, kest, kerr,
+      kaxis, kpest, kperr);
+}
+
+void launch_refine(cudaStream_t st, int64_t m, const double* est, const double* raw,
+                   const double* pest, double* out) {
+  if (m > 0) k_refine<<<grid_for(m, 256), 256, 0, st>>>(m, est, raw, pest, out);
+}
+void launch_classify(cudaStream_t st, int64_t m, const double* est, const double* err,
+                     double tau, int enabled, uint8_t* flags) {
+  if (m > 0) k_classify<<<grid_for(m, 256), 256, 0, st>>>(m, est, err, tau, enabled, flags);
+}
+void launch_apply_threshold(cudaStream_t st, int64_t m, const double* err, double t,
+                            uint8_t* flags) {
+  if (m > 0) k_apply_threshold<<<grid_for(m, 256), 256, 0, st>>>(m, err, t, flags);
+}
+void launch_serial_volume(cudaStream_t st, int n, int64_t m, int64_t cap, const double* len,
+                          const uint8_t* flag, int which, double* out) {
+  k_serial_volume<<<1, 1, 0, st>>>(n, m, cap, len, flag, which, out);
+}
+void launch_math(cudaStream_t st, int which, int64_t m, const double* x, double* y) {
+  if (m > 0) k_math<<<grid_for(m, 256), 256, 0, st>>>(which, m, x, y);
+}
+
+void launch_call_integrand(cudaStream_t st, int fid, int n, int64_t m, const double* x,
+                           const IntegrandParams& ip, double* y) {
+  if (m <= 0) return;
+  const unsigned g = grid_for(m, 128);
+  switch (fid) {
+    case 1: k_call<F1><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 2: k_call<F2><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 3: k_call<F3><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 4: k_call<F4><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 5: k_call<F5><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 6: k_call<F6><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 7: k_call<F7><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 8: k_call<F8><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 100: k_call<TConst><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 101: k_call<TMonomial><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 102: k_call<TRough><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 103: k_call<TNanBox><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 104: k_call<TPocket><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 105: k_call<TCosSum><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    case 106: k_call<TExpSq><<<g, 128, 0, st>>>(n, m, x, ip, y); break;
+    default: break;
+  }
+}
+
+}  // namespace pgn

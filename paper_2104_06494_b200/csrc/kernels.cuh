@@ -1,0 +1,94 @@
+// Region-store kernels around k_evaluate: deterministic block folds, the
+// pairwise tree, min/max, threshold probes, fused filter+bisect, uniform split.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "evaluate.cuh"
+
+namespace pgn {
+
+// reduce.cpp:10 -- block size of the deterministic sums.  Every global fp64
+// sum in the loop is "serial inside fixed 2048-element blocks, then a fixed
+// pairwise tree over the block partials" (reduce.cpp:13-64); reproducing that
+// exactly is what makes v, e, v_f, e_f and the threshold sums bit-identical.
+constexpr int64_t kBlock = 2048;
+
+inline int64_t nblocks_of(int64_t m) { return (m + kBlock - 1) / kBlock; }
+
+// Scalars produced by k_finalize (device) and copied to pinned host memory.
+struct FoldScalars {
+  double sum[4];
+  int64_t count;
+  int64_t pad;
+};
+
+using EvalKernel = void (*)(const EvalParams, const uint64_t*, const double*);
+
+// ---- launchers (kernels.cu) ------------------------------------------------
+// uniform_split of the unit cube (geometry.cpp:83-112), axis-major.
+void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap, double* low,
+                          double* len, const double* lower, const double* step);
+
+// Post-evaluation block folds: q0 = sum est, q1 = sum err,
+// q2 = sum est[flag==0] (+ count flag==1), q3 = sum err[flag==0].
+void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
+                      const uint8_t* flag, double* part, int64_t* cnt);
+
+// Threshold probe (classify.cpp:63-70): cand = flag & !(err < t);
+// q0 = sum err[cand==0], q1 = sum est[cand==0], count(cand==1) -> cnt.
+// Candidates are never materialised: k_split re-derives them from t.
+void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const double* err,
+                  const uint8_t* flag, double* part, int64_t* cnt);
+void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,
+                       const double* err, uint8_t* out);
+
+// Generic fold of one array with optional mask (block_sum / block_sum_where).
+void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t* flag,
+                     int which, double* part, int64_t* cnt);
+
+// Pairwise trees over nq partial arrays (stride nblk) + exclusive scan of cnt.
+void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
+                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out);
+
+// min_max over err (reduce.cpp:74-82).  out[0] = min, out[1] = max, as doubles.
+void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,
+                   double* out);
+
+// Fused filter (classify.cpp:97-129) + bisect (geometry.cpp:114-143): region
+// j with flag 1 and rank k among the kept writes children 2k, 2k+1 into dst.
+void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
+                  const uint8_t* flag, int use_t, double t, const int64_t* offsets,
+                  const double* est,
+                  const double* err, const uint8_t* axis, const double* low, const double* len,
+                  double* dlow, double* dlen, double* dpest, double* dperr);
+
+// Compaction only (filter() for the batch API).
+void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
+                    const int64_t* offsets, const double* low, const double* len,
+                    const double* est, const double* err, const int32_t* axis,
+                    const double* pest, const double* perr, double* klow, double* klen,
+                    double* kest, double* kerr, int32_t* kaxis, double* kpest, double* kperr);
+
+// Elementwise helpers for the batch API.
+void launch_refine(cudaStream_t st, int64_t m, const double* est, const double* raw,
+                   const double* pest, double* out);
+void launch_classify(cudaStream_t st, int64_t m, const double* est, const double* err,
+                     double tau, int enabled, uint8_t* flags);
+void launch_apply_threshold(cudaStream_t st, int64_t m, const double* err, double t,
+                            uint8_t* flags);
+void launch_serial_volume(cudaStream_t st, int n, int64_t m, int64_t cap, const double* len,
+                          const uint8_t* flag, int which, double* out);
+void launch_math(cudaStream_t st, int which, int64_t m, const double* x, double* y);
+void launch_call_integrand(cudaStream_t st, int fid, int n, int64_t m, const double* x,
+                           const IntegrandParams& ip, double* y);
+
+// Device copies of the glibc tables.
+const uint64_t* device_exp_table();
+const double* device_sincos_table();
+
+// k_evaluate dispatch (eval_*.cu): nullptr if (fid, n, mode) is unsupported.
+EvalKernel lookup_evaluate(int fid, int n, int mode);
+
+}  // namespace pgn
