@@ -1,0 +1,320 @@
+#!/usr/bin/env python3
+"""PAGANI hot-path benchmark (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): the 8D Genz suite f1..f6 at
+epsrel in {1e-3, 1e-4, 1e-5, 1e-6}, tau_abs=1e-20, it_max=100,
+max_regions=2^22 (the reference defaults), relative filtering off for f1 only
+(bfcub_cli.cpp:77-78).  One "step" = the 24 integrate() calls.
+
+  value   region-evals/s over the step, device time: the CUDA-event span of
+          each integrate() on the library's stream (inputs: none -- the
+          region list is generated and kept in HBM by the library)
+  e2e     the same metric through the public Python API / C ABI, host wall
+          clock, including every host<->device copy (bounds/config in, the
+          per-iteration scalar read-backs and the result out)
+  roofline  k_evaluate (FP64 CUDA-core bound): algorithmic FLOPs
+          (paper_2104_06494_b200/roofline.py) / its summed
+          CUDA-event time, against an FP64 DFMA peak measured live on the box
+  cpu_baseline  the unmodified reference library (oracle/_ref) on the box's
+          host cores on a bounded sample of the same workload
+
+--impl reference runs that reference library (all host threads) on the
+bounded sample for every step.  Multi-GPU (torchrun): each rank runs the
+workload on its own GPU (weak scaling, "replicas") -- see DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-tolerance (s) & region-evals/s, 8D Genz f1–f6, at 1/2/4/8 B200"
+UNIT = "region-evals/s"
+DIM = 8
+TAUS = (1e-3, 1e-4, 1e-5, 1e-6)
+FIDS = (1, 2, 3, 4, 5, 6)
+# Bounded CPU sample of the same workload: f1..f6 8D tau=1e-3, first 9 iterations.
+CPU_SAMPLE_IT_MAX = 9
+CPU_SAMPLE_DESC = "f1..f6 8D tau=1e-3 with it_max=9 (first 9 PAGANI iterations of each)"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def workload(cases=None):
+    """All (fid, tau) of the suite, or a subset like "f4@1e-3,f1@1e-3"."""
+    if cases:
+        out = []
+        for c in cases.split(","):
+            f, t = c.split("@")
+            out.append((int(f.strip().lstrip("f")), float(t)))
+        return out
+    return [(fid, tau) for fid in FIDS for tau in TAUS]
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append((float(p[1]), float(p[2]), p[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm_max = max(r[1] for r in rows)
+        loaded = [r for r in rows if r[0] > 0.3 * sm_max] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": sm_max,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- ours -------
+def run_ours(args, rank, world, local_rank):
+    import paper_2104_06494_b200 as pg
+    from paper_2104_06494_b200 import roofline
+
+    torch = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    device = local_rank
+
+    def barrier_sync():
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        return float(t.item())
+
+    mode = args.mode
+    cases = workload(args.cases)
+
+    def one_step(profile):
+        rs = []
+        for fid, tau in cases:
+            cfg = pg.Config(tau_rel=tau, rel_filtering_enabled=(fid != 1), max_regions=args.max_regions,
+                            mode=mode, device=device, profile=profile)
+            rs.append((fid, tau, pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(DIM), cfg)))
+        return rs
+
+    for _ in range(args.warmup):
+        one_step(True)
+
+    peak_tflops, peak_mhz = pg.api.fp64_peak(device, 1.0)
+
+    clocks = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(device)).split(",")[0])
+                          if os.environ.get("CUDA_VISIBLE_DEVICES", "").isdigit() else device)
+    clocks.start()
+    barrier_sync()
+    t_wall0 = time.perf_counter()
+    steps = []
+    for _ in range(args.steps):
+        steps.append(one_step(True))
+    barrier_sync()
+    t_wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+
+    dev_ms = sum(r.device_ms for st in steps for _, _, r in st)
+    region_evals = sum(r.region_evals for st in steps for _, _, r in st)
+    eval_ms = sum(r.kernel_ms["evaluate"] for st in steps for _, _, r in st)
+    eval_launches = sum(r.kernel_launches["evaluate"] for st in steps for _, _, r in st)
+    flops = sum(r.region_evals * roofline.region_flops(fid, DIM) for st in steps
+                for fid, _, r in st)
+    launches = sum(sum(r.kernel_launches.values()) for st in steps for _, _, r in st)
+    h2d = sum(r.h2d_bytes for st in steps for _, _, r in st) / args.steps
+    d2h = sum(r.d2h_bytes for st in steps for _, _, r in st) / args.steps
+
+    # e2e: the public API's host wall clock over the same K steps
+    dev_s_max = max_over_ranks(dev_ms / 1e3)
+    wall_s_max = max_over_ranks(t_wall)
+    evals_all = sum_over_ranks(region_evals)
+    value = evals_all / dev_s_max
+    e2e_value = evals_all / wall_s_max
+
+    if rank != 0:
+        return
+    per_case = []
+    for fid, tau, r in steps[-1]:
+        per_case.append({"f": f"f{fid}", "tau": tau, "status": str(r.status),
+                         "it": r.iterations, "regions": r.regions_generated,
+                         "estimate": r.estimate, "time_to_result_s": r.device_ms / 1e3})
+    achieved = flops / (eval_ms / 1e3) / 1e12 if eval_ms > 0 else 0.0
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "ncu_evaluate_summary.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_s_max * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's fixed-parameter Genz integrands (deterministic, no dataset)",
+        "config": {"workload": "genz_8d_suite: f1..f6 x tau in {1e-3,1e-4,1e-5,1e-6}, n=8, "
+                               "tau_abs=1e-20, it_max=100, rel filter off for f1",
+                   "max_regions": args.max_regions, "mode": mode,
+                   "l2": "working set > L2: each run streams a region store of up to 1.1 GB",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "roofline": {"bound": "fp64", "kernel": "k_evaluate_sep", "achieved": achieved,
+                     "peak": peak_tflops, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tflops if peak_tflops else None,
+                     "traffic": traffic,
+                     "peak_source": f"measured live: DFMA microbenchmark (pagani_fp64_peak) at "
+                                    f"{peak_mhz:.0f} MHz; MEASURED_PEAKS.json has no FP64 entry",
+                     "flops_model": "SURVEY.md 8(d) F(f,n), paper_2104_06494_b200/roofline.py",
+                     "eval_ms": eval_ms / args.steps, "eval_launches": eval_launches // args.steps,
+                     "eval_share_of_step": eval_ms / dev_ms if dev_ms else None,
+                     "kernel_ms_per_step": {k: round(sum(r.kernel_ms[k] for st in steps
+                                                         for _, _, r in st) / args.steps, 3)
+                                            for k in ("evaluate", "fold", "finalize", "minmax",
+                                                      "probe", "split", "init")}},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "time_to_tolerance_s": {f"{c['f']}@{c['tau']:g}": round(c["time_to_result_s"], 6)
+                                for c in per_case},
+        "outcomes": per_case,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- reference --
+def ref_sample(ref, make_config):
+    """One bounded sample of the workload on the reference library."""
+    evals = 0
+    t0 = time.perf_counter()
+    for fid in FIDS:
+        cfg = make_config(tau_rel=1e-3, it_max=CPU_SAMPLE_IT_MAX, rel_filtering_enabled=(fid != 1))
+        r = ref.integrate(fid, DIM, cfg)
+        evals += r.eval_count // ((1 << DIM) + 2 * DIM * (DIM - 1) + 4 * DIM + 1)
+    return evals, time.perf_counter() - t0
+
+
+def cpu_baseline():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from ref_ctypes import Ref, make_config
+    ref = Ref()
+    evals, secs = ref_sample(ref, make_config)
+    return {"value": evals / secs, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": CPU_SAMPLE_DESC + f"; {evals} region-evals in {secs:.1f} s, OpenMP "
+                      f"threads = all {os.cpu_count()} host cores"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        from ref_ctypes import Ref, make_config
+        ref = Ref()
+    except Exception as e:  # the reference is compiled in-tree; this should not happen
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
+        return
+    for _ in range(args.warmup):
+        ref_sample(ref, make_config)
+    tot_e, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        e, s = ref_sample(ref, make_config)
+        tot_e += e
+        tot_s += s
+    value = tot_e / tot_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's fixed-parameter Genz integrands (deterministic)",
+        "config": {"workload": "genz_8d_suite (bounded sample per step: " + CPU_SAMPLE_DESC + ")",
+                   "max_regions": 1 << 22, "mode": "reference CPU (bfcub, OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(),
+                         "kind": "reference", "sample": CPU_SAMPLE_DESC},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="parity", choices=["parity", "fast"])
+    ap.add_argument("--max-regions", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cases", default=None,
+                    help="profiling subset, e.g. f4@1e-3 (the default is the whole suite)")
+    args = ap.parse_args()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

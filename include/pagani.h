@@ -163,6 +163,7 @@ typedef struct pagani_result {
   int64_t region_evals;                        /* sum over iterations of batch sizes */
   int64_t peak_regions;
   int64_t h2d_bytes, d2h_bytes;
+  double device_ms; /* CUDA-event span on the driver stream: first kernel -> last */
 } pagani_result;
 
 /* One row per iteration (the BFCUB_TRACE point, driver.cpp:174-182, in full
@@ -263,6 +264,11 @@ int pagani_math_cos(int64_t m, const double* x, double* y, int32_t on_device);
 /* Evaluate a builtin integrand at host points (m x n), on the device. */
 int pagani_call_integrand(const pagani_integrand* f, int n, int64_t m, const double* x,
                           double* y);
+
+/* FP64 roofline denominator: a DFMA-chain microbenchmark over every SM of
+ * `device` for about `seconds`; returns the achieved FP64 TFLOP/s (2 flops
+ * per DFMA) and the SM clock (MHz) seen by the kernel. */
+int pagani_fp64_peak(int device, double seconds, double* tflops, double* sm_mhz);
 
 /* ---- multi-GPU (one process per GPU) ----------------------
  * unique_id: 128 bytes produced by pagani_comm_unique_id() on rank 0 and

@@ -89,7 +89,8 @@ class Result(C.Structure):
                 ("kernel_ms", C.c_double * PAGANI_N_KERNEL_SLOTS),
                 ("kernel_launches", C.c_int64 * PAGANI_N_KERNEL_SLOTS),
                 ("region_evals", C.c_int64), ("peak_regions", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("device_ms", C.c_double)]
 
 
 class ThresholdResult(C.Structure):
@@ -142,6 +143,7 @@ SIGNATURES = {
     "pagani_math_exp": (C.c_int, [C.c_int64, _D, _D, C.c_int32]),
     "pagani_math_cos": (C.c_int, [C.c_int64, _D, _D, C.c_int32]),
     "pagani_call_integrand": (C.c_int, [C.POINTER(Integrand), C.c_int, C.c_int64, _D, _D]),
+    "pagani_fp64_peak": (C.c_int, [C.c_int, C.c_double, _D, _D]),
     "pagani_comm_unique_id": (C.c_int, [_U8]),
     "pagani_comm_init_rank": (C.c_int, [_U8, C.c_int, C.c_int, C.c_int,
                                         C.POINTER(C.c_void_p)]),

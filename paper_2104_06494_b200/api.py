@@ -188,6 +188,7 @@ class IntegrationResult:
     peak_regions: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    device_ms: float = 0.0
     trace: Optional[list] = None
 
 
@@ -304,7 +305,8 @@ def integrate(f, bounds: Bounds, config: Optional[Config] = None,
         kernel_ms={k: out.kernel_ms[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         kernel_launches={k: out.kernel_launches[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         region_evals=out.region_evals, peak_regions=out.peak_regions,
-        h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, trace=rows if trace else None)
+        h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, device_ms=out.device_ms,
+        trace=rows if trace else None)
 
 
 def check_termination(v, e, v_f, e_f, tau_rel, tau_abs) -> bool:  # driver.hpp:71-72
@@ -563,6 +565,13 @@ def glibc_cos(x, on_device=True):
     y = np.empty_like(x)
     N.check(_lib().pagani_math_cos(len(x), _dp(x), _dp(y), int(on_device)))
     return y
+
+
+def fp64_peak(device: int = 0, seconds: float = 1.0):
+    """Measured FP64 DFMA peak of `device`: (TFLOP/s, SM MHz seen by the kernel)."""
+    t, mhz = C.c_double(), C.c_double()
+    N.check(_lib().pagani_fp64_peak(device, seconds, C.byref(t), C.byref(mhz)))
+    return t.value, mhz.value
 
 
 def device_count() -> int:

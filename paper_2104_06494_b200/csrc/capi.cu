@@ -152,8 +152,8 @@ int pagani_evaluate_batch(const pagani_integrand* f, int n, int64_t m, const dou
   return guarded([&] {
     if (n < 1 || n > 16) throw std::invalid_argument("evaluate_batch: dimension mismatch");
     const pgn::DeviceIntegrand di = pgn::resolve_integrand(f);
-    const pgn::EvalKernel k = pgn::lookup_evaluate(di.fid, n, mode);
-    if (!k) throw pgn::UnsupportedError("no device kernel for this integrand/dimension");
+    const pgn::EvalLaunch k = pgn::lookup_evaluate(di.fid, n, mode);
+    if (!k.fn) throw pgn::UnsupportedError("no device kernel for this integrand/dimension");
     const pgn::RuleOrbits rule = pgn::build_rule_orbits(n);
     if (eval_count) *eval_count = m * rule.point_count;
     if (m <= 0) return;
@@ -182,8 +182,7 @@ int pagani_evaluate_batch(const pagani_integrand* f, int n, int64_t m, const dou
       for (int o = 0; o < 5; ++o) ep.w[kk][o] = rule.w[kk][o];
     for (int i = 0; i < 4; ++i) ep.gen[i] = rule.gen[i];
     ep.ip = di.params;
-    k<<<static_cast<unsigned>((m + pgn::kEvalThreads - 1) / pgn::kEvalThreads), pgn::kEvalThreads,
-        0, c.st>>>(ep, pgn::device_exp_table(), pgn::device_sincos_table());
+    pgn::launch_evaluate(k, c.st, ep);
     PGN_CK(cudaGetLastError());
     d2h(estimates, est.p, m, c.st);
     d2h(raw_errors, raw.p, m, c.st);

@@ -193,6 +193,7 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
 
   cudaStream_t st = ws.st;
   launch_minmax(st, m, d_err, ws.mm_keys.p, ws.mm_out.p);
+  r.minmax_launches = 3;
   PGN_CK(cudaMemcpyAsync(ws.h_mm, ws.mm_out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   PGN_CK(cudaStreamSynchronize(st));
   const double min_err = ws.h_mm[0], max_err = ws.h_mm[1];
@@ -272,11 +273,14 @@ void validate_config(const pagani_config& c) {  // driver.cpp:35-41
     throw std::invalid_argument("Config: max_regions must be >= 2 * init_target");
 }
 
+// Event slots: 0/1 probe loop, 2/3 whole-call span, 4.. per-kernel marks.
+constexpr size_t kSpanBegin = 2, kSpanEnd = 3, kFirstMark = 4;
+
 struct KTimer {
   Workspace& ws;
   bool on;
   std::vector<std::pair<int, std::pair<size_t, size_t>>> spans;
-  size_t next = 2;  // events 0/1 belong to the probe loop
+  size_t next = kFirstMark;
   KTimer(Workspace& w, bool o) : ws(w), on(o) {}
   size_t mark() {
     if (!on) return 0;
@@ -295,7 +299,7 @@ struct KTimer {
       out->kernel_ms[s.first] += ms;
     }
     spans.clear();
-    next = 2;
+    next = kFirstMark;
   }
 };
 
@@ -312,8 +316,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   const DeviceIntegrand di = resolve_integrand(f);
   if (cfg.mode != PAGANI_MODE_PARITY && cfg.mode != PAGANI_MODE_FAST)
     throw std::invalid_argument("Config: unknown mode");
-  const EvalKernel eval_k = lookup_evaluate(di.fid, n, cfg.mode);
-  if (!eval_k) throw UnsupportedError("no device kernel for this integrand/dimension");
+  const EvalLaunch eval_k = lookup_evaluate(di.fid, n, cfg.mode);
+  if (!eval_k.fn) throw UnsupportedError("no device kernel for this integrand/dimension");
   if (cfg.comm) throw UnsupportedError("multi-GPU communicator passed to the 1-GPU driver");
 
   std::memset(out, 0, sizeof(*out));
@@ -346,6 +350,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   const int64_t cap = ws.cap;
   const bool prof = cfg.profile != 0;
   KTimer kt(ws, prof);
+  cudaEvent_t ev_begin = ws.event(kSpanBegin), ev_end = ws.event(kSpanEnd);
+  PGN_CK(cudaEventRecord(ev_begin, st));
 
   {  // uniform split of the unit cube
     double lo[kMaxDim], step[kMaxDim];
@@ -381,8 +387,6 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     ep.map_len[a] = dom_len[a];
   }
   ep.ip = di.params;
-  const uint64_t* g_exp = device_exp_table();
-  const double* g_sc = device_sincos_table();
 
   Limits lim;
   lim.direction_change_limit = cfg.direction_change_limit;
@@ -414,8 +418,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     ep.len = ws.len[cur].p;
     ep.refine = (it > 1 && cfg.refiner == PAGANI_REFINER_TWO_LEVEL) ? 1 : 0;
     const size_t k0 = kt.mark();
-    eval_k<<<static_cast<unsigned>((m + kEvalThreads - 1) / kEvalThreads), kEvalThreads, 0, st>>>(
-        ep, g_exp, g_sc);
+    launch_evaluate(eval_k, st, ep);
     PGN_CK(cudaGetLastError());
     const size_t k1 = kt.mark();
     kt.span(PAGANI_K_EVALUATE, k0, k1);
@@ -492,6 +495,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
                            acc_e + acc_ef, acc_e, m, cfg.tau_rel, lim, prof ? &pms : nullptr);
       out->kernel_ms[PAGANI_K_PROBE] += pms;
       out->kernel_launches[PAGANI_K_PROBE] += tr.attempts;
+      out->kernel_launches[PAGANI_K_FINALIZE] += tr.attempts;
+      out->kernel_launches[PAGANI_K_MINMAX] += tr.minmax_launches;
       out->d2h_bytes += tr.attempts * sizeof(FoldScalars);
       if (out->n_events < PAGANI_MAX_EVENTS) {
         pagani_threshold_event& ev = out->events[out->n_events];
@@ -578,7 +583,13 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     if (m > out->peak_regions) out->peak_regions = m;
   }
   if (!done) finish(PAGANI_MAX_ITERATIONS, cfg.it_max);
+  PGN_CK(cudaEventRecord(ev_end, st));
   PGN_CK(cudaStreamSynchronize(st));
+  {
+    float span = 0;
+    PGN_CK(cudaEventElapsedTime(&span, ev_begin, ev_end));
+    out->device_ms = span;
+  }
   kt.collect(out);
   out->wall_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_wall0).count();

@@ -90,6 +90,7 @@ struct ThresholdOutcome {
   int64_t finished_count = 0;
   int attempts = 0, direction_changes = 0;
   double fin_v = 0.0;  // sum of estimates where candidate == 0 (valid on success)
+  int minmax_launches = 0;  // kernels launched by min_max (0 or 3)
 };
 
 struct Limits {

@@ -5,11 +5,11 @@
 namespace pgn {
 
 template <int N>
-static EvalKernel pick_f1(int mode) {
-  return mode ? &k_evaluate_sep<N, F1, 1> : &k_evaluate_sep<N, F1, 0>;
+static EvalLaunch pick_f1(int mode) {
+  return {mode ? &k_evaluate_sep<N, F1, 1> : &k_evaluate_sep<N, F1, 0>, eval_smem_bytes<N>()};
 }
 
-EvalKernel lookup_eval_f1(int n, int mode) {
+EvalLaunch lookup_eval_f1(int n, int mode) {
   switch (n) {
     case 1: return pick_f1<1>(mode);
     case 2: return pick_f1<2>(mode);
@@ -27,7 +27,7 @@ EvalKernel lookup_eval_f1(int n, int mode) {
     case 14: return pick_f1<14>(mode);
     case 15: return pick_f1<15>(mode);
     case 16: return pick_f1<16>(mode);
-    default: return nullptr;
+    default: return {};
   }
 }
 

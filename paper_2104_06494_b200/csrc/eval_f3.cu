@@ -5,11 +5,11 @@
 namespace pgn {
 
 template <int N>
-static EvalKernel pick_f3(int mode) {
-  return mode ? &k_evaluate_sep<N, F3, 1> : &k_evaluate_sep<N, F3, 0>;
+static EvalLaunch pick_f3(int mode) {
+  return {mode ? &k_evaluate_sep<N, F3, 1> : &k_evaluate_sep<N, F3, 0>, eval_smem_bytes<N>()};
 }
 
-EvalKernel lookup_eval_f3(int n, int mode) {
+EvalLaunch lookup_eval_f3(int n, int mode) {
   switch (n) {
     case 1: return pick_f3<1>(mode);
     case 2: return pick_f3<2>(mode);
@@ -27,7 +27,7 @@ EvalKernel lookup_eval_f3(int n, int mode) {
     case 14: return pick_f3<14>(mode);
     case 15: return pick_f3<15>(mode);
     case 16: return pick_f3<16>(mode);
-    default: return nullptr;
+    default: return {};
   }
 }
 

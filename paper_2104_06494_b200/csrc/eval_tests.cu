@@ -1,25 +1,29 @@
 // k_evaluate instantiations for the reference unit-test integrands
 // (generic full-point path, runtime dimension).
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "kernels.cuh"
 
 namespace pgn {
 
 template <class F>
-static EvalKernel pick(int mode) {
-  return mode ? &k_evaluate_gen<F, 1> : &k_evaluate_gen<F, 0>;
+static EvalLaunch pick(int mode) {
+  return {mode ? &k_evaluate_gen<F, 1> : &k_evaluate_gen<F, 0>, 0};
 }
 
-EvalKernel lookup_eval_f1(int, int);
-EvalKernel lookup_eval_f2(int, int);
-EvalKernel lookup_eval_f3(int, int);
-EvalKernel lookup_eval_f4(int, int);
-EvalKernel lookup_eval_f5(int, int);
-EvalKernel lookup_eval_f6(int, int);
-EvalKernel lookup_eval_f7(int, int);
-EvalKernel lookup_eval_f8(int, int);
+EvalLaunch lookup_eval_f1(int, int);
+EvalLaunch lookup_eval_f2(int, int);
+EvalLaunch lookup_eval_f3(int, int);
+EvalLaunch lookup_eval_f4(int, int);
+EvalLaunch lookup_eval_f5(int, int);
+EvalLaunch lookup_eval_f6(int, int);
+EvalLaunch lookup_eval_f7(int, int);
+EvalLaunch lookup_eval_f8(int, int);
 
-EvalKernel lookup_evaluate(int fid, int n, int mode) {
-  if (n < 1 || n > 16) return nullptr;
+EvalLaunch lookup_evaluate(int fid, int n, int mode) {
+  if (n < 1 || n > 16) return {};
   switch (fid) {
     case 1: return lookup_eval_f1(n, mode);
     case 2: return lookup_eval_f2(n, mode);
@@ -36,8 +40,23 @@ EvalKernel lookup_evaluate(int fid, int n, int mode) {
     case 104: return pick<TPocket>(mode);
     case 105: return pick<TCosSum>(mode);
     case 106: return pick<TExpSq>(mode);
-    default: return nullptr;
+    default: return {};
   }
+}
+
+void launch_evaluate(const EvalLaunch& k, cudaStream_t st, const EvalParams& ep) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> configured;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (k.smem > 0 && configured.insert({dev, reinterpret_cast<const void*>(k.fn)}).second)
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(k.fn),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem));
+  }
+  const unsigned grid = static_cast<unsigned>((ep.m + kEvalThreads - 1) / kEvalThreads);
+  k.fn<<<grid, kEvalThreads, k.smem, st>>>(ep, device_exp_table(), device_sincos_table());
 }
 
 }  // namespace pgn

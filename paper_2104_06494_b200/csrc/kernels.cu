@@ -77,68 +77,88 @@ __device__ __forceinline__ double serial_fold(const double* __restrict__ x,
   return s;
 }
 
-__global__ void k_fold_eval(int64_t m, int64_t nblk, const double* __restrict__ est,
-                            const double* __restrict__ err, const uint8_t* __restrict__ flag,
-                            double* part, int64_t* cnt) {
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t b = gid >> 2;
-  const int q = static_cast<int>(gid & 3);
-  if (b >= nblk) return;
-  const int64_t lo = b * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
-  const double* x = (q & 1) ? err : est;
-  double s;
-  if (q < 2) {
-    s = serial_fold<false>(x, nullptr, 0, lo, hi, nullptr);
-  } else {
-    int64_t active = 0;  // entries with flag != 0
-    s = serial_fold<true>(x, flag, 0, lo, hi, &active);
-    if (q == 2) cnt[b] = active;
+// One CTA per 2048-block: the block is staged in shared memory with
+// coalesced loads, then the strict serial folds run from smem (the chain is a
+// dependent DADD sequence, so the only thing that matters is that each step
+// waits on DADD latency, not on a global load).  The est chains and the err
+// chains run on lane 0 of two different warps so they issue in parallel.
+constexpr int kFoldThreads = 256;
+
+struct FoldSmem {
+  double est[kBlock];
+  double err[kBlock];
+  uint8_t flag[kBlock];
+};
+
+__device__ __forceinline__ int64_t stage_block(FoldSmem& S, const double* __restrict__ est,
+                                               const double* __restrict__ err,
+                                               const uint8_t* __restrict__ flag, int64_t lo,
+                                               int cnt, bool need_est, double t, bool probe) {
+  int active = 0;
+  for (int i = threadIdx.x; i < kBlock; i += kFoldThreads) {
+    bool a = false;
+    if (i < cnt) {
+      const double e = __ldg(err + lo + i);
+      uint8_t f = __ldg(flag + lo + i);
+      if (probe) f = (f && !(e < t)) ? 1 : 0;  // candidate (classify.cpp:63-66)
+      S.err[i] = e;
+      S.flag[i] = f;
+      if (need_est) S.est[i] = __ldg(est + lo + i);
+      a = f != 0;
+    }
+    active += __syncthreads_count(a);
   }
-  part[q * nblk + b] = s;
+  return active;
 }
 
-__global__ void k_probe(int64_t m, int64_t nblk, double t, const double* __restrict__ est,
-                        const double* __restrict__ err, const uint8_t* __restrict__ flag,
-                        double* part, int64_t* cnt) {
-  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t b = gid >> 2;
-  const int q = static_cast<int>(gid & 3);
-  if (b >= nblk || q == 3) return;
-  const int64_t lo = b * kBlock, hi = lo + kBlock < m ? lo + kBlock : m;
-  // candidate = active & !(err < t)   (classify.cpp:29-35, 63-66)
-  // q0: sum err where candidate == 0  (classify.cpp:70)
-  // q1: sum est where candidate == 0  (classify.cpp:104, used if accepted)
-  // q2: count candidate == 1          (classify.cpp:68)
-  const double* x = q == 1 ? est : err;
-  double s = 0.0;
-  int64_t c = 0;
-  int64_t i = lo;
-  for (; i + 8 <= hi; i += 8) {
-    double v[8], e[8];
-    uint8_t g[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      e[u] = __ldg(err + i + u);
-      v[u] = q == 1 ? __ldg(x + i + u) : e[u];
-      g[u] = __ldg(flag + i + u);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool c1 = g[u] && !(e[u] < t);
-      c += c1;
-      if (q < 2) s = P_ADD(s, c1 ? 0.0 : v[u]);
-    }
+// q0 = sum est, q1 = sum err, q2 = sum est[flag==0], q3 = sum err[flag==0],
+// cnt = #flag==1   (reduce.cpp:31-64 via driver.cpp:145-146, classify.cpp:104-108)
+__global__ void __launch_bounds__(kFoldThreads)
+    k_fold_eval(int64_t m, int64_t nblk, const double* __restrict__ est,
+                const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
+                int64_t* cnt) {
+  __shared__ FoldSmem S;
+  const int64_t b = blockIdx.x;
+  const int64_t lo = b * kBlock;
+  const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
+  const int64_t active = stage_block(S, est, err, flag, lo, n, true, 0.0, false);
+  if ((threadIdx.x & 31) != 0 || threadIdx.x >= 64) {
+    if (threadIdx.x == 64) cnt[b] = active;
+    return;
   }
-  for (; i < hi; ++i) {
-    const double e = __ldg(err + i);
-    const bool c1 = __ldg(flag + i) && !(e < t);
-    c += c1;
-    if (q < 2) s = P_ADD(s, c1 ? 0.0 : (q == 1 ? __ldg(est + i) : e));
+  const double* x = threadIdx.x == 0 ? S.est : S.err;
+  double all = 0.0, fin = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) {
+    const double v = x[i];
+    all = P_ADD(all, v);
+    fin = P_ADD(fin, S.flag[i] ? 0.0 : v);
   }
-  if (q < 2)
-    part[q * nblk + b] = s;
-  else
-    cnt[b] = c;
+  const int q = threadIdx.x == 0 ? 0 : 1;
+  part[q * nblk + b] = all;
+  part[(q + 2) * nblk + b] = fin;
+}
+
+// Threshold probe: q0 = sum err[cand==0], q1 = sum est[cand==0],
+// cnt = #cand==1 with cand = flag & !(err < t)  (classify.cpp:63-70, 104-105).
+__global__ void __launch_bounds__(kFoldThreads)
+    k_probe(int64_t m, int64_t nblk, double t, const double* __restrict__ est,
+            const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
+            int64_t* cnt) {
+  __shared__ FoldSmem S;
+  const int64_t b = blockIdx.x;
+  const int64_t lo = b * kBlock;
+  const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
+  const int64_t active = stage_block(S, est, err, flag, lo, n, true, t, true);
+  if ((threadIdx.x & 31) != 0 || threadIdx.x >= 64) {
+    if (threadIdx.x == 64) cnt[b] = active;
+    return;
+  }
+  const double* x = threadIdx.x == 0 ? S.err : S.est;
+  double fin = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) fin = P_ADD(fin, S.flag[i] ? 0.0 : x[i]);
+  part[(threadIdx.x == 0 ? 0 : 1) * nblk + b] = fin;
 }
 
 __global__ void k_candidates(int64_t m, double t, const uint8_t* flag, const double* err,
@@ -449,14 +469,16 @@ void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const doubl
                       const uint8_t* flag, double* part, int64_t* cnt) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
-  k_fold_eval<<<grid_for(nblk * 4, 128), 128, 0, st>>>(m, nblk, est, err, flag, part, cnt);
+  k_fold_eval<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, est, err, flag,
+                                                                     part, cnt);
 }
 
 void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const double* err,
                   const uint8_t* flag, double* part, int64_t* cnt) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
-  k_probe<<<grid_for(nblk * 4, 128), 128, 0, st>>>(m, nblk, t, est, err, flag, part, cnt);
+  k_probe<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, t, est, err, flag, part,
+                                                                 cnt);
 }
 
 void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,

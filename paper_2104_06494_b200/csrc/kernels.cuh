@@ -25,6 +25,10 @@ struct FoldScalars {
 };
 
 using EvalKernel = void (*)(const EvalParams, const uint64_t*, const double*);
+struct EvalLaunch {
+  EvalKernel fn = nullptr;
+  size_t smem = 0;  // dynamic shared memory bytes
+};
 
 // ---- launchers (kernels.cu) ------------------------------------------------
 // uniform_split of the unit cube (geometry.cpp:83-112), axis-major.
@@ -88,7 +92,9 @@ void launch_call_integrand(cudaStream_t st, int fid, int n, int64_t m, const dou
 const uint64_t* device_exp_table();
 const double* device_sincos_table();
 
-// k_evaluate dispatch (eval_*.cu): nullptr if (fid, n, mode) is unsupported.
-EvalKernel lookup_evaluate(int fid, int n, int mode);
+// k_evaluate dispatch (eval_*.cu): fn == nullptr if (fid, n, mode) is unsupported.
+EvalLaunch lookup_evaluate(int fid, int n, int mode);
+// Launch k_evaluate for m regions on `st` (sets the dynamic-smem attribute once).
+void launch_evaluate(const EvalLaunch& k, cudaStream_t st, const EvalParams& ep);
 
 }  // namespace pgn
