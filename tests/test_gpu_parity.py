@@ -1,0 +1,390 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the
+unmodified reference library (oracle/_ref) and the committed goldens.
+
+Bar: bit-exact for everything (estimates, errors, split axes, counts, traces)
+in parity mode; fast mode within 1e-12 relative with identical decisions.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import bits, load_golden, unhex
+from ref_ctypes import make_config
+
+pytestmark = pytest.mark.gpu
+
+TOL_FAST = 1e-12  # north_star: final integral within 1e-12 relative
+
+
+def cfg_pair(pg, tau, relf=True, **extra):
+    """The same configuration for the product and the reference shim."""
+    refkw = dict(extra)
+    pgkw = dict(extra)
+    if "refiner" in pgkw:
+        pgkw["refiner"] = {0: "two_level", 1: "identity"}[pgkw["refiner"]]
+    lim = {k: pgkw.pop(k) for k in ("attempt_limit", "direction_change_limit", "p_max_start",
+                                    "p_max_step", "p_max_cap") if k in pgkw}
+    if lim:
+        pgkw["threshold_limits"] = pg.ThresholdLimits(**lim)
+    return (pg.Config(tau_rel=tau, rel_filtering_enabled=relf, **pgkw),
+            make_config(tau_rel=tau, rel_filtering_enabled=relf, **refkw))
+
+
+def integrand(pg, fid, params=None):
+    return pg.Integrand(fid, params or [])
+
+
+def assert_same_result(res, want):
+    assert res.estimate == unhex(want["estimate"]) or (
+        np.isnan(res.estimate) and np.isnan(unhex(want["estimate"])))
+    assert res.errorest == unhex(want["errorest"]) or (
+        np.isinf(res.errorest) and np.isinf(unhex(want["errorest"])))
+    assert str(res.status) == want["status"]
+    assert res.iterations == want["iterations"]
+    assert res.regions_generated == want["regions_generated"]
+    assert res.eval_count == want["eval_count"]
+
+
+def assert_same_trace(rows, want_rows, name):
+    assert len(rows) == len(want_rows), name
+    for got, want in zip(rows, want_rows):
+        for k, v in want.items():
+            w = unhex(v)
+            g = got[k]
+            assert g == w or (isinstance(w, float) and w != w and g != g), (name, got["it"], k, g, w)
+
+
+# ----------------------------------------------------------- libm ----------
+def test_device_glibc_exp_cos_bit_exact(pg, gpu, ref):
+    rng = np.random.default_rng(5)
+    for fn, libm, xs in (
+            (pg.glibc_exp, ref.lib.ref_libm_exp,
+             np.concatenate([rng.uniform(-1300, 720, 2_000_000), rng.uniform(-45, 45, 2_000_000),
+                             [0.0, -0.0, -745.2, -708.3, -1024.0, -1075.0, 709.8, 710.0, np.inf,
+                              -np.inf, np.nan, -512.0, 1e-300]])),
+            (pg.glibc_cos, ref.lib.ref_libm_cos,
+             np.concatenate([rng.uniform(-40, 40, 2_000_000), rng.uniform(0, 140, 2_000_000),
+                             [0.0, -0.0, 1e-9, 0.855469, 2.426265, np.pi / 2, 36.0, np.inf,
+                              np.nan]]))):
+        got = fn(xs, on_device=True)
+        want = np.empty_like(xs)
+        libm(C.c_int64(len(xs)), xs.ctypes.data_as(C.POINTER(C.c_double)),
+             want.ctypes.data_as(C.POINTER(C.c_double)))
+        assert np.array_equal(bits(got), bits(want))
+
+
+# ------------------------------------------------------ evaluate ----------
+@pytest.mark.parametrize("fid", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_evaluate_batch_bit_exact(pg, gpu, ref, fid):
+    rng = np.random.default_rng(100 + fid)
+    for n in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12):
+        m = 700 if n <= 10 else 64
+        lows = rng.uniform(0.0, 0.6, size=(m, n))
+        lens = rng.uniform(0.01, 0.4, size=(m, n))
+        lens[:5] = 2.0 ** -rng.integers(1, 30, size=(5, n))  # deep bisection lengths
+        est, raw, axes, cnt = pg.evaluate_batch(pg.Integrand(fid), lows, lens)
+        e2, r2, a2, c2 = ref.evaluate_batch(fid, lows, lens)
+        assert np.array_equal(bits(est), bits(e2)), (fid, n)
+        assert np.array_equal(bits(raw), bits(r2)), (fid, n)
+        assert np.array_equal(axes, a2), (fid, n)
+        assert cnt == c2
+
+
+def test_evaluate_batch_n16_and_unit_cube_splits(pg, gpu, ref):
+    for fid in (3, 4, 5):
+        lows, lens = ref.uniform_split([0.0] * 16, [1.0] * 16, 1)
+        a = pg.evaluate_batch(pg.Integrand(fid), lows, lens)
+        b = ref.evaluate_batch(fid, lows, lens)
+        assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(a[2], b[2])
+    for fid in range(1, 9):
+        lows, lens = ref.uniform_split([0.0] * 5, [1.0] * 5, 6)  # 5D initial batch
+        a = pg.evaluate_batch(pg.Integrand(fid), lows, lens)
+        b = ref.evaluate_batch(fid, lows, lens)
+        assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(bits(a[1]), bits(b[1]))
+        assert np.array_equal(a[2], b[2])
+
+
+def test_evaluate_matches_golden_batches(pg, gpu):
+    for name, b in load_golden("batch.json").items():
+        lows = np.array([[unhex(v) for v in r] for r in b["lows"]])
+        lens = np.array([[unhex(v) for v in r] for r in b["lengths"]])
+        est, raw, axes, cnt = pg.evaluate_batch(pg.Integrand(b["fid"]), lows, lens)
+        assert np.array_equal(bits(est), bits([unhex(v) for v in b["est"]])), name
+        assert np.array_equal(bits(raw), bits([unhex(v) for v in b["raw"]])), name
+        assert axes.tolist() == b["axes"] and cnt == b["eval_count"], name
+
+
+TEST_INTEGRANDS = [(100, [1.0]), (100, [-2.5]), (101, [1, 2, 0, 3]), (102, [40.0, 1.0, 2.0]),
+                   (102, [50.0, 2.0, 2.0]), (103, [0.6, 0.6]), (103, [0.8, -1.0]), (104, [0.95]),
+                   (105, [7.25, 0.7, 1.9, 2.6, 1.1]), (106, [])]
+
+
+@pytest.mark.parametrize("fid,params", TEST_INTEGRANDS)
+def test_unit_test_integrands_bit_exact(pg, gpu, ref, fid, params):
+    rng = np.random.default_rng(fid)
+    for n in (3, 4):
+        lows = rng.uniform(0.0, 0.7, size=(300, n))
+        lens = rng.uniform(0.01, 0.3, size=(300, n))
+        a = pg.evaluate_batch(pg.Integrand(fid, params), lows, lens)
+        b = ref.evaluate_batch(fid, lows, lens, params=params)
+        assert np.array_equal(bits(a[0]), bits(b[0])) and np.array_equal(bits(a[1]), bits(b[1]))
+        assert np.array_equal(a[2], b[2])
+
+
+def test_rule_known_answers_on_device(pg, gpu):
+    """test_rule.cpp:82-254 through the device evaluator."""
+    for n in (1, 2, 4, 8):  # constant: exact estimate, ~zero raw error
+        b = pg.uniform_split(pg.Bounds.unit_cube(n), 1)
+        est, raw, _, cnt = pg.evaluate_batch(pg.Integrand.constant(1.0), b.lows, b.lengths)
+        assert abs(est[0] - 1.0) <= 1e-14 and raw[0] < 1e-13 and cnt == pg.rule_point_count(n)
+    import itertools
+    for n in (1, 2, 3):  # degree-7 exactness
+        b = pg.uniform_split(pg.Bounds.unit_cube(n), 1)
+        for alpha in itertools.product(range(8), repeat=n):
+            if sum(alpha) > 7:
+                continue
+            est, _, _, _ = pg.evaluate_batch(pg.Integrand.monomial(alpha), b.lows, b.lengths)
+            exact = 1.0
+            for e in alpha:
+                exact /= e + 1
+            assert abs(est[0] - exact) <= 1e-12 * exact, alpha
+    b = pg.uniform_split(pg.Bounds.unit_cube(1), 1)
+    est, raw, _, _ = pg.evaluate_batch(pg.Integrand.monomial([9]), b.lows, b.lengths)
+    assert est[0] != 0.1 and raw[0] > 0.0
+    # zero axis signal -> widest extent (axis 1)
+    lens = np.array([[0.25, 1.0, 0.5]])
+    _, _, axes, _ = pg.evaluate_batch(pg.Integrand.pocket(0.95), 1.0 - lens, lens)
+    assert axes[0] == 1
+    # NaN -> est 0, raw +inf
+    b = pg.uniform_split(pg.Bounds.unit_cube(2), 2)
+    est, raw, _, _ = pg.evaluate_batch(pg.Integrand.nan_box(0.6, 0.6), b.lows, b.lengths)
+    assert np.isinf(raw).sum() >= 1 and (est[np.isinf(raw)] == 0.0).all()
+    # split axis invariant under positive scaling (seeded freqs as in test_rule.cpp)
+    fr = np.random.default_rng(21).uniform(0.5, 3.0, size=4)
+    b = pg.uniform_split(pg.Bounds.unit_cube(4), 2)
+    a1 = pg.evaluate_batch(pg.Integrand.cos_sum(1.0, fr), b.lows, b.lengths)[2]
+    a2 = pg.evaluate_batch(pg.Integrand.cos_sum(7.25, fr), b.lows, b.lengths)[2]
+    assert np.array_equal(a1, a2)
+
+
+# ------------------------------------------------- batch functions --------
+def test_refine_classify_threshold_bit_exact(pg, gpu, ref):
+    rng = np.random.default_rng(42)
+    m = 200_000
+    est = rng.normal(size=m)
+    raw = np.abs(rng.normal(size=m)) * 10.0 ** rng.integers(-12, 0, size=m)
+    raw[::97] = 0.0
+    raw[::1001] = np.inf
+    pest = np.repeat(rng.normal(size=m // 2) * 2, 2)
+    perr = np.abs(rng.normal(size=m))
+    a = pg.two_level_refine(est, raw, pest, perr)
+    b = ref.two_level_refine(est, raw, pest, perr)
+    assert np.array_equal(bits(a), bits(b))
+    for tau, en in ((1e-3, True), (1e-6, True), (1e-3, False)):
+        assert np.array_equal(pg.rel_err_classify(est, a, tau, en),
+                              ref.rel_err_classify(est, a, tau, en))
+    assert np.array_equal(pg.apply_threshold(a, 1e-6), (a >= 1e-6).astype(np.uint8))
+    # reference known answers (test_errorest.cpp:10-29, test_classify.cpp:114-146)
+    out = pg.two_level_refine([3.0, 1.0], [0.08, 0.02], [4.0, 4.0], [0.5, 0.5])
+    assert abs(out[0] - 0.01) < 1e-15 and abs(out[1] - 0.0025) < 1e-15
+    with pytest.raises(ValueError):
+        pg.two_level_refine([1.0], [1.0], [1.0], [1.0])
+    r = pg.threshold_classify([1, 1, 1, 1], [9, 9, 1, 1], 0.0, 100.0, 20.0, 4, 1e-3)
+    assert not r.success and r.flags.tolist() == [1, 1, 1, 1]
+    r = pg.threshold_classify([1, 1, 1, 1], [9, 1, 1, 1], 0.0, 100.0, 12.0, 4, 1e-3)
+    assert r.success and r.finished_count == 3 and r.discarded_error == 3.0
+    assert r.flags.tolist() == [1, 0, 0, 0] and r.discarded_error <= r.budget_limit
+    assert not pg.threshold_classify([1, 1], [5, 5], 1e6, 10.0, 10.0, 2, 1e-3).success
+
+
+def test_threshold_trace_oracle_instances(pg, gpu, ref):
+    """test_classify.cpp:148-182: 300 random instances (seeded), plus large ones."""
+    rng = np.random.default_rng(2024)
+    for trial in range(300):
+        m = 2 + int(rng.uniform() * 40) if trial < 280 else int(rng.integers(3000, 300_000))
+        e = 10.0 ** (-6.0 * rng.uniform(size=m))
+        act = (rng.uniform(size=m) < 0.8).astype(np.uint8)
+        v_tot = rng.uniform() * 10
+        e_it = float(e.sum())
+        e_tot = e_it * (1 + rng.uniform())
+        tau = 10.0 ** (-1.0 - 3.0 * rng.uniform())
+        a = pg.threshold_classify(act, e, v_tot, e_tot, e_it, m, tau)
+        b = ref.threshold_classify(act, e, v_tot, e_tot, e_it, m, tau)
+        assert a.success == b["success"] and np.array_equal(a.flags, b["flags"]), trial
+        assert (a.threshold, a.discarded_error, a.budget_limit, a.finished_count, a.attempts,
+                a.direction_changes) == (b["threshold"], b["discarded_error"], b["budget_limit"],
+                                         b["finished_count"], b["attempts"],
+                                         b["direction_changes"]), trial
+
+
+def test_filter_bisect_split_sums_bit_exact(pg, gpu, ref):
+    rng = np.random.default_rng(11)
+    for n, m in ((1, 3), (3, 5000), (8, 70_000)):
+        lows = rng.uniform(0, 0.5, size=(m, n))
+        lens = 2.0 ** -rng.integers(1, 20, size=(m, n)).astype(float)
+        est = rng.normal(size=m)
+        err = np.abs(rng.normal(size=m))
+        axis = rng.integers(0, n, size=m).astype(np.int32)
+        pest, perr = rng.normal(size=m), np.abs(rng.normal(size=m))
+        flags = (rng.uniform(size=m) < 0.6).astype(np.uint8)
+        batch = pg.RegionBatch(lows, lens, est, err, axis, pest, perr)
+        f = pg.filter(batch, flags)
+        g = ref.filter(lows, lens, est, err, axis, pest, perr, flags)
+        assert f.kept.count == g["kept"]
+        assert (f.finished_estimate, f.finished_error, f.finished_volume) == (
+            g["finished_estimate"], g["finished_error"], g["finished_volume"])
+        for k1, k2 in (("lows", "lows"), ("lengths", "lengths"), ("estimates", "estimates"),
+                       ("errors", "errors"), ("parent_estimates", "parent_estimates"),
+                       ("parent_errors", "parent_errors")):
+            assert np.array_equal(bits(getattr(f.kept, k1)), bits(g[k2])), k1
+        assert np.array_equal(f.kept.split_axis, g["split_axis"])
+        c = pg.bisect(batch, 1 << 22)
+        d = ref.bisect(lows, lens, est, err, axis)
+        assert np.array_equal(bits(c.lows), bits(d[0])) and np.array_equal(bits(c.lengths), bits(d[1]))
+        assert np.array_equal(bits(c.parent_estimates), bits(d[2]))
+        assert np.array_equal(bits(c.parent_errors), bits(d[3]))
+    with pytest.raises(AssertionError):  # logic_error: doubling beyond the cap
+        pg.bisect(pg.RegionBatch(np.zeros((2, 1)), np.ones((2, 1))), 3)
+    for lo, hi, d in (([0, 0], [1, 1], 3), ([0, -1], [2, 1], 2), ([-1.5, 0.25, 3], [2, 0.5, 7], 5)):
+        u = pg.uniform_split(pg.Bounds(lo, hi), d)
+        v = ref.uniform_split(lo, hi, d)
+        assert np.array_equal(bits(u.lows), bits(v[0])) and np.array_equal(bits(u.lengths), bits(v[1]))
+    with pytest.raises(RuntimeError):
+        pg.uniform_split(pg.Bounds([0, 0, 0], [1, 1, 1]), 100, 1000)
+    x = rng.normal(size=5_000_001) * 10.0 ** rng.integers(-5, 5, size=5_000_001)
+    fl = (rng.uniform(size=len(x)) < 0.3).astype(np.uint8)
+    assert pg.block_sum(x) == ref.block_sum(x)
+    assert pg.block_sum_where(x, fl, 0) == ref.block_sum_where(x, fl, 0)
+    assert pg.block_sum_where(x, fl, 1) == ref.block_sum_where(x, fl, 1)
+    assert pg.count_flags(fl, 1) == int(fl.sum())
+    assert pg.min_max(x) == (x.min(), x.max())
+    assert pg.block_sum([]) == 0.0
+
+
+# ------------------------------------------------------ integrate ---------
+def test_integrate_matches_golden_traces(pg, gpu):
+    """Every per-iteration field of the reference's own trace, bit for bit."""
+    for name, case in load_golden("traces.json").items():
+        cfg, _ = cfg_pair(pg, case["tau"], case["rel_filter"], **case["extra"])
+        res = pg.integrate(integrand(pg, case["fid"], case["params"]),
+                           pg.Bounds.unit_cube(case["n"]), cfg, trace=True)
+        assert_same_result(res, case["result"])
+        assert_same_trace(res.trace, case["trace"], name)
+        want_ev = case["result"]["threshold_events"]
+        assert len(res.threshold_events) == len(want_ev), name
+        for e, w in zip(res.threshold_events, want_ev):
+            assert (e.iteration, e.success, e.batch_size, e.finished_count,
+                    e.discarded_error, e.budget_limit) == (
+                w["iteration"], w["success"], w["batch_size"], w["finished_count"],
+                unhex(w["discarded_error"]), unhex(w["budget_limit"])), name
+
+
+def test_integrate_matches_reference_finals_8d(pg, gpu):
+    """BASELINE 8D configs at the reference default cap (2^22): the reference's
+    final results (tests/golden/finals.json, minutes of CPU each)."""
+    for name, want in load_golden("finals.json").items():
+        cfg = pg.Config(tau_rel=want["tau"], rel_filtering_enabled=want["fid"] != 1)
+        res = pg.integrate(pg.Integrand(want["fid"]), pg.Bounds.unit_cube(want["n"]), cfg)
+        assert_same_result(res, want)
+        assert len(res.threshold_events) == want["n_events"], name
+
+
+MORE_CASES = [
+    ("mapped_xy", 101, 2, 1e-6, True, {}, [1, 1], ([0, 1], [2, 3])),
+    ("mapped_f4", 4, 3, 1e-4, True, {}, None, ([-1, 0, 0.25], [1, 2, 0.75])),
+    ("identity_refiner", 5, 3, 1e-6, True, {"refiner": 1}, None, None),
+    ("it_max_1", 3, 4, 1e-9, True, {"it_max": 1}, None, None),
+    ("tight_limits", 4, 3, 1e-8, True, {"max_regions": 1 << 11, "init_target": 1 << 8,
+                                        "attempt_limit": 3, "direction_change_limit": 1},
+     None, None),
+    ("init_subdiv", 6, 4, 1e-5, True, {"init_subdiv": 3}, None, None),
+]
+
+
+@pytest.mark.parametrize("name,fid,n,tau,relf,extra,params,bounds", MORE_CASES)
+def test_integrate_matches_live_reference(pg, gpu, ref, name, fid, n, tau, relf, extra, params,
+                                          bounds):
+    cfg, rcfg = cfg_pair(pg, tau, relf, **extra)
+    b = pg.Bounds(*bounds) if bounds else pg.Bounds.unit_cube(n)
+    res = pg.integrate(integrand(pg, fid, params), b, cfg)
+    want = ref.integrate(fid, n, rcfg, lower=b.lower, upper=b.upper, params=params)
+    assert (res.estimate, res.errorest, str(res.status), res.iterations, res.regions_generated,
+            res.eval_count) == (want.estimate, want.errorest, want.status, want.iterations,
+                                want.regions_generated, want.eval_count), name
+    if bounds is None:
+        _, rows = ref.trace(fid, n, rcfg, params=params)
+        res2 = pg.integrate(integrand(pg, fid, params), b, cfg, trace=True)
+        assert res2.trace == rows
+
+
+def test_driver_known_answers(pg, gpu):
+    """test_driver.cpp:22-154 through the GPU driver."""
+    r = pg.integrate(pg.Integrand.constant(1.0), pg.Bounds.unit_cube(3),
+                     pg.Config(tau_rel=1e-3, init_subdiv=2))
+    assert r.status == pg.Status.Converged and r.iterations == 1 and r.regions_generated == 8
+    assert abs(r.estimate - 1.0) < 1e-13 and r.errorest < 1e-10
+    r = pg.integrate(pg.Integrand.rough(40.0, 1, 2.0), pg.Bounds.unit_cube(2),
+                     pg.Config(tau_rel=1e-12, rel_filtering_enabled=False, init_subdiv=2, it_max=4))
+    assert r.status == pg.Status.MaxIterations and r.regions_generated == 60
+    assert r.eval_count == 60 * 17
+    r = pg.integrate(pg.Integrand.monomial([1, 1]), pg.Bounds([0, 1], [2, 3]),
+                     pg.Config(tau_rel=1e-6))
+    assert r.status == pg.Status.Converged and abs(r.estimate - 8.0) <= 1e-10 * 8.0
+    r = pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(2),
+                     pg.Config(tau_rel=1e-9, max_regions=1 << 10, init_target=1 << 9))
+    assert r.threshold_events
+    r = pg.integrate(pg.Integrand.nan_box(0.8), pg.Bounds.unit_cube(2),
+                     pg.Config(tau_rel=1e-6, max_regions=1 << 10, init_target=1 << 8, it_max=12))
+    assert r.status != pg.Status.Converged and np.isinf(r.errorest)
+    r = pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(3),
+                     pg.Config(tau_rel=5e-7, max_regions=1 << 12, init_target=1 << 10))
+    for ev in r.threshold_events:
+        if ev.success:
+            assert ev.retained_fraction() < 0.5
+            assert ev.discarded_error <= ev.budget_limit * (1 + 1e-12)
+    with pytest.raises(RuntimeError):  # runtime_error: d^n exceeds max_regions
+        pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(3),
+                     pg.Config(init_subdiv=100, max_regions=1000))
+
+
+def test_validate_invariants_mode(pg, gpu, ref):
+    cfg, rcfg = cfg_pair(pg, 1e-3, True, validate_invariants=True)
+    res = pg.integrate(pg.integrand_by_id("f3"), pg.Bounds.unit_cube(3), cfg)
+    want = ref.integrate(3, 3, rcfg)
+    assert (res.estimate, res.iterations) == (want.estimate, want.iterations)
+
+
+def test_determinism_and_workspace_reuse(pg, gpu):
+    cfg = pg.Config(tau_rel=1e-3)
+    a = pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(5), cfg)
+    b = pg.integrate(pg.integrand_by_id("f6"), pg.Bounds.unit_cube(6), cfg)
+    c = pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(5), cfg)
+    assert (a.estimate, a.errorest, a.regions_generated) == (c.estimate, c.errorest,
+                                                              c.regions_generated)
+    assert b.estimate != a.estimate
+
+
+def test_fast_mode_within_tolerance(pg, gpu):
+    for fid, n, tau in ((4, 5, 1e-3), (3, 8, 1e-3), (5, 5, 1e-4), (2, 6, 1e-3), (6, 6, 1e-3)):
+        p = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n), pg.Config(tau_rel=tau))
+        f = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n),
+                         pg.Config(tau_rel=tau, mode="fast"))
+        assert (f.status, f.iterations, f.regions_generated) == (p.status, p.iterations,
+                                                                  p.regions_generated)
+        assert abs(f.estimate - p.estimate) <= TOL_FAST * abs(p.estimate)
+
+
+def test_large_batch_properties(pg, gpu):
+    """At the full default cap: the region count identity and the trace's
+    accounting hold exactly (sizes too large for the CPU oracle in a test)."""
+    res = pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(8),
+                       pg.Config(tau_rel=1e-6), trace=True)
+    ms = [r["m"] for r in res.trace]
+    assert sum(ms) == res.region_evals == res.eval_count // 401
+    assert res.regions_generated == sum(ms)
+    for prev, nxt in zip(res.trace, res.trace[1:]):
+        assert nxt["m"] == 2 * prev["kept"]
+        assert nxt["v_f"] == prev["v_f"] + prev["fin_v"]
+        assert nxt["e_f"] == prev["e_f"] + prev["fin_e"]
+    assert max(ms) <= 1 << 22

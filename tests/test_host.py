@@ -1,0 +1,191 @@
+"""CPU-only tests of the product library: symbols, host logic, the host build
+of the glibc restatement, the rule builder, API validation, loud failure
+without a GPU.  Reference = the unmodified reference library (oracle/_ref)."""
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, bits
+
+HEADER = os.path.join(ROOT, "include", "pagani.h")
+LIB = os.path.join(ROOT, "paper_2104_06494_b200", "libpagani_b200.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(pagani_\w+)\s*\(",
+                                 src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 30
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True,
+                         check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+
+
+def test_library_loads_and_binds_all_signatures(pg):
+    from paper_2104_06494_b200 import _native
+    lib = _native.load()
+    for name in declared_functions():
+        assert name in _native.SIGNATURES, name
+        assert getattr(lib, name) is not None
+    assert lib.pagani_abi_version() == 1
+
+
+def test_rule_weights_bit_identical_to_reference(pg, ref):
+    """build_rule (rule.cpp:166-349) restated in x87 long double: every orbit
+    weight and generator equals the reference's double, n = 1..16."""
+    for n in range(1, 17):
+        w, g, pts, ws = pg.build_rule(n)
+        rpts, rws, _ = ref.build_rule(n)
+        assert pts.shape == rpts.shape
+        assert np.array_equal(bits(pts), bits(rpts)), n
+        assert np.array_equal(bits(ws), bits(rws)), n
+
+
+def test_rule_point_counts_and_weight_sums(pg):
+    """test_rule.cpp:58-80."""
+    assert pg.rule_point_count(1) == 7
+    assert pg.rule_point_count(2) == 17
+    assert pg.rule_point_count(8) == 401
+    for bad in (0, 17):
+        with pytest.raises(ValueError):
+            pg.build_rule(bad)
+    for n in range(1, 9):
+        _, _, _, ws = pg.build_rule(n)
+        sums = [math.fsum(ws[k]) for k in range(5)]
+        assert abs(sums[0] - 1.0) < 1e-14
+        for k in range(1, 5):
+            assert abs(sums[k]) < 1e-14
+
+
+def test_host_glibc_restatement_matches_libm(pg, ref):
+    """glibc_math.cuh compiled for the host equals the platform libm bit for
+    bit (the same source runs on the device)."""
+    import ctypes as C
+    rng = np.random.default_rng(11)
+    xs = np.concatenate([rng.uniform(-1300, 720, 400_000), rng.uniform(-50, 50, 400_000),
+                         rng.uniform(-1e-3, 1e-3, 50_000),
+                         np.array([0.0, -0.0, 1e-300, -745.2, -708.3, -1024.0, -1023.9, -1075.0,
+                                   709.8, 710.0, -np.inf, np.inf, np.nan, -600.0, -512.0])])
+    mine = pg.glibc_exp(xs, on_device=False)
+    libm = np.empty_like(xs)
+    ref.lib.ref_libm_exp(C.c_int64(len(xs)), xs.ctypes.data_as(C.POINTER(C.c_double)),
+                         libm.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(bits(mine), bits(libm))
+    cs = np.concatenate([rng.uniform(-40, 40, 400_000), rng.uniform(0, 3, 400_000),
+                         rng.uniform(-1e6, 1e6, 50_000),
+                         np.array([0.0, -0.0, 1e-9, 0.855469, 2.426265, np.pi / 2, 36.0, np.inf,
+                                   np.nan])])
+    mine = pg.glibc_cos(cs, on_device=False)
+    libm = np.empty_like(cs)
+    ref.lib.ref_libm_cos(C.c_int64(len(cs)), cs.ctypes.data_as(C.POINTER(C.c_double)),
+                         libm.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(bits(mine), bits(libm))
+
+
+def test_scalar_helpers_match_reference(pg, ref):
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        a = float(rng.uniform(-1, 1) * 10.0 ** int(rng.integers(-12, 12)))
+        b = a * (1 + float(rng.normal()) * 10 ** -float(rng.integers(1, 16)))
+        d = int(rng.integers(0, 19))
+        assert pg.digits_converged(a, b, d) == ref.digits_converged(a, b, d)
+    for tau in (1e-3, 8e-6, 1e-9, 0.5, 2.0, 1e-17, 1e-30, 3.3e-4):
+        assert pg.Config(tau_rel=tau).convergence_digits() == ref.convergence_digits(tau)
+    for n in range(1, 17):
+        for t in (1 << 9, 1 << 10, 1 << 14, 1 << 20):
+            assert pg.initial_subdivisions(n, t) == ref.initial_subdivisions(n, t)
+    # test_geometry.cpp:165-170, test_driver.cpp:34-59
+    assert pg.initial_subdivisions(8, 1 << 14) == 3
+    assert pg.initial_subdivisions(2, 1 << 14) == 128
+    assert pg.initial_subdivisions(14, 1 << 14) == 2
+    assert pg.initial_subdivisions(15, 1 << 14) == 1
+    assert pg.check_termination(2.0, 1e-3, 0.0, 0.0, 1e-3, 1e-20)
+    assert pg.check_termination(0.0, 1e-21, 0.0, 0.0, 1e-3, 1e-20)
+    assert not pg.check_termination(1.0, 0.5, 0.0, 0.0, 1e-3, 1e-20)
+    assert pg.digits_converged(1.23456, 1.23461, 4)
+    assert not pg.digits_converged(1.0, 1.1, 3)
+    assert pg.digits_converged(0.0, 0.0, 5)
+    assert not pg.digits_converged(-1.0, 1.0, 2)
+    assert not pg.digits_converged(float("nan"), 1.0, 3)
+    assert pg.Config().convergence_digits() == 3
+    assert pg.Config(tau_rel=8e-6).convergence_digits() == 6
+
+
+def test_api_validation_mirrors_reference(pg):
+    """geometry.cpp:9-23 and driver.cpp:35-41 error behaviour."""
+    with pytest.raises(ValueError):
+        pg.Bounds([0, 1], [1, 1])
+    with pytest.raises(ValueError):
+        pg.Bounds([0], [1, 2])
+    with pytest.raises(ValueError):
+        pg.Bounds([0.0] * 17, [1.0] * 17)
+    with pytest.raises(ValueError):
+        pg.Bounds([0.0], [float("inf")])
+    with pytest.raises(ValueError):
+        pg.Config(tau_rel=0.0).validate()
+    with pytest.raises(ValueError):
+        pg.Config(max_regions=1 << 14).validate()
+    pg.Config().validate()
+    with pytest.raises(NotImplementedError):  # host callables: no CPU fallback
+        pg.integrate(lambda x, n: 1.0, pg.Bounds.unit_cube(2))
+    with pytest.raises(ValueError):
+        pg.integrand_by_id("f9")
+    assert pg.known_integrand("f4") and not pg.known_integrand("g1")
+    b = pg.Bounds([0, 1], [2, 3])
+    assert b.volume() == 4.0 and not b.is_unit_cube() and pg.Bounds.unit_cube(3).is_unit_cube()
+
+
+def test_c_abi_rejects_host_function_pointer(pg):
+    """A PAGANI_HOST_FN integrand fails with PAGANI_E_UNSUPPORTED, never a CPU path."""
+    import ctypes as C
+    from paper_2104_06494_b200 import _native as N
+    lib = N.load()
+    f = N.Integrand()
+    lib.pagani_integrand_builtin(C.byref(f), 4, None, 0)
+    f.kind = N.PAGANI_HOST_FN
+    cfg = N.Config()
+    lib.pagani_config_default(C.byref(cfg))
+    lo = (C.c_double * 2)(0.0, 0.0)
+    hi = (C.c_double * 2)(1.0, 1.0)
+    out = N.Result()
+    rc = lib.pagani_integrate(C.byref(f), 2, lo, hi, C.byref(cfg), C.byref(out))
+    assert rc == N.PAGANI_E_UNSUPPORTED
+    assert b"no CPU fallback" in lib.pagani_last_error()
+
+
+def test_invalid_config_rejected_before_touching_the_device(pg):
+    with pytest.raises(ValueError):
+        pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(2), pg.Config(tau_rel=-1.0))
+    with pytest.raises(ValueError):
+        pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(2), pg.Config(it_max=0))
+
+
+def test_device_calls_fail_loudly_without_gpu(pg):
+    """On a host without a GPU the product raises; it never computes on the CPU."""
+    if pg.device_count() > 0:
+        pytest.skip("a GPU is present")
+    from paper_2104_06494_b200._native import CudaUnavailable
+    with pytest.raises(CudaUnavailable):
+        pg.integrate(pg.integrand_by_id("f4"), pg.Bounds.unit_cube(3))
+    with pytest.raises(CudaUnavailable):
+        pg.glibc_exp(np.array([1.0]), on_device=True)
+    with pytest.raises(CudaUnavailable):
+        pg.evaluate_batch(pg.integrand_by_id("f4"), np.zeros((2, 2)), np.ones((2, 2)))
+
+
+def test_roofline_flop_model():
+    from paper_2104_06494_b200 import roofline
+    assert roofline.rule_points(8) == 401
+    assert roofline.ipow_muls(9) == 6 and roofline.ipow_muls(11) == 7 and roofline.ipow_muls(7) == 6
+    assert roofline.region_flops(4, 8) == 401 * (16 + 10 + 24 + 1 + 20) + 88 + 2
