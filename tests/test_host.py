@@ -189,3 +189,27 @@ def test_roofline_flop_model():
     assert roofline.rule_points(8) == 401
     assert roofline.ipow_muls(9) == 6 and roofline.ipow_muls(11) == 7 and roofline.ipow_muls(7) == 6
     assert roofline.region_flops(4, 8) == 401 * (16 + 10 + 24 + 1 + 20) + 88 + 2
+
+
+def _build_cpp_example(tmp_path):
+    exe = tmp_path / "cpp_dropin"
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cpp_dropin.cpp"),
+                    "-L" + os.path.dirname(LIB), "-lpagani_b200",
+                    "-Wl,-rpath," + os.path.dirname(LIB), "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_mirror_header_compiles_links_and_runs_host_parts(tmp_path):
+    """include/pagani.hpp: reference-style C++ (bfcub:: names via the alias)
+    builds against the C ABI and links the in-tree library."""
+    exe = _build_cpp_example(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert "digits=3 d(8)=3 N(8)=401" in out
+
+
+@pytest.mark.gpu
+def test_cpp_mirror_header_integrates_on_gpu(tmp_path):
+    exe = _build_cpp_example(tmp_path)
+    out = subprocess.run([str(exe), "run"], capture_output=True, text=True, check=True).stdout
+    assert "f4 5D: 1.7913125097877638e-06" in out and "converged it=11 regions=7959712" in out
