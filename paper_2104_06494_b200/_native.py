@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libpagani_b200.so")
+LIB_PATH = os.environ.get("PAGANI_LIB") or os.path.join(PKG_DIR, "libpagani_b200.so")
 REPO_ROOT = os.path.dirname(PKG_DIR)
 
 PAGANI_OK = 0

@@ -57,6 +57,12 @@ void Workspace::ensure(int n_, int64_t cap_) {
   cnt_probe.alloc(nb);
   off_eval.alloc(nb);
   off_probe.alloc(nb);
+  blk_done.alloc(nb);
+  PGN_CK(cudaMemset(blk_done.p, 0, nb * sizeof(int)));
+  mm_blk.alloc(2 * nb);
+  part_multi.alloc(2 * kMaxProbes * nb);
+  cnt_multi.alloc(kMaxProbes * nb);
+  scratch_multi.alloc(2 * 2 * kMaxProbes * nb + 2);
   if (!d_sc.p) {
     d_sc.alloc(2);
     mm_keys.alloc(2);
@@ -66,6 +72,8 @@ void Workspace::ensure(int n_, int64_t cap_) {
     d_tmp.alloc(4);
     PGN_CK(cudaMallocHost(&h_sc, 2 * sizeof(FoldScalars)));
     PGN_CK(cudaMallocHost(&h_mm, 4 * sizeof(double)));
+    d_probe.alloc(1);
+    PGN_CK(cudaMallocHost(&h_probe, sizeof(ProbeScalars)));
   }
   n = nn;
   cap = nc;
@@ -85,6 +93,7 @@ Workspace::~Workspace() {
   for (auto e : ev) cudaEventDestroy(e);
   if (h_sc) cudaFreeHost(h_sc);
   if (h_mm) cudaFreeHost(h_mm);
+  if (h_probe) cudaFreeHost(h_probe);
   if (st) cudaStreamDestroy(st);
 }
 
@@ -183,7 +192,7 @@ int initial_subdivisions(int n, int64_t init_target) {  // geometry.cpp:67-81
 ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
-                                  const Limits& lim, double* probe_ms) {
+                                  const Limits& lim, double* probe_ms, const double* minmax) {
   ThresholdOutcome r;
   if (s_it <= 0) return r;
   const double e_budget = e_tot - std::fabs(v_tot) * tau_rel;
@@ -192,54 +201,92 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
   if (!(e_budget > 0.0)) return r;
 
   cudaStream_t st = ws.st;
-  launch_minmax(st, m, d_err, ws.mm_keys.p, ws.mm_out.p);
-  r.minmax_launches = 3;
-  PGN_CK(cudaMemcpyAsync(ws.h_mm, ws.mm_out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  PGN_CK(cudaStreamSynchronize(st));
-  const double min_err = ws.h_mm[0], max_err = ws.h_mm[1];
+  double min_err, max_err;
+  if (minmax) {
+    min_err = minmax[0];
+    max_err = minmax[1];
+  } else {
+    launch_minmax(st, m, d_err, ws.mm_keys.p, ws.mm_out.p);
+    r.minmax_launches = 3;
+    PGN_CK(cudaMemcpyAsync(ws.h_mm, ws.mm_out.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PGN_CK(cudaStreamSynchronize(st));
+    min_err = ws.h_mm[0];
+    max_err = ws.h_mm[1];
+  }
   double t = e_it / static_cast<double>(s_it);
 
+  // The search is a walk down a binary tree: from threshold t the next probe
+  // is (t + max)/2 if too few regions finish, (t + min)/2 if too much error
+  // would be discarded (classify.cpp:82-89).  p_max only changes acceptance,
+  // never the t sequence, so a pass evaluates the whole depth-4 subtree (15
+  // thresholds) and the host replays the reference's sequential decisions on
+  // the results -- identical outcomes, up to 4 probes per round trip.
   enum Dir { kNone, kTowardMax, kTowardMin };
   Dir last = kNone;
   const int64_t nblk = nblocks_of(m);
-  while (r.attempts < lim.attempt_limit) {
-    ++r.attempts;
+  bool done = false;
+  while (!done && r.attempts < lim.attempt_limit) {
+    ProbeSet ps{};
+    ps.T = kMaxProbes;
+    ps.t[0] = t;
+    for (int k = 0; 2 * k + 2 < kMaxProbes; ++k) {
+      ps.t[2 * k + 1] = (ps.t[k] + max_err) * 0.5;
+      ps.t[2 * k + 2] = (ps.t[k] + min_err) * 0.5;
+    }
     cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
     if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
-    launch_probe(st, m, t, d_est, d_err, d_flag, ws.part_probe.p, ws.cnt_probe.p);
-    launch_finalize(st, nblk, 2, ws.part_probe.p, ws.cnt_probe.p, ws.off_probe.p, ws.scratch.p,
-                    ws.d_sc.p + 1);
+    launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
+                       ws.scratch_multi.p, ws.d_probe.p);
     if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
-    PGN_CK(cudaMemcpyAsync(ws.h_sc + 1, ws.d_sc.p + 1, sizeof(FoldScalars),
-                           cudaMemcpyDeviceToHost, st));
+    PGN_CK(cudaMemcpyAsync(ws.h_probe, ws.d_probe.p, sizeof(ProbeScalars), cudaMemcpyDeviceToHost,
+                           st));
     PGN_CK(cudaStreamSynchronize(st));
+    ++r.passes;
     if (probe_ms) {
       float ms = 0;
       PGN_CK(cudaEventElapsedTime(&ms, e0, e1));
       *probe_ms += ms;
     }
-    const FoldScalars sc = ws.h_sc[1];
-    const int64_t inactive = s_it - sc.count;
-    const bool memory_ok = 2 * inactive > s_it;
-    const double discarded = sc.sum[0];
-    if (memory_ok && discarded <= p_max * e_budget) {
-      r.success = true;
-      r.threshold = t;
-      r.discarded = discarded;
-      r.budget_limit = p_max * e_budget;
-      r.finished_count = inactive;
-      r.fin_v = sc.sum[1];
-      return r;
+    const ProbeScalars& pr = *ws.h_probe;
+    int node = 0;
+    for (;;) {
+      ++r.attempts;
+      const int64_t inactive = s_it - pr.count[node];
+      const bool memory_ok = 2 * inactive > s_it;
+      const double discarded = pr.err_sum[node];
+      if (memory_ok && discarded <= p_max * e_budget) {
+        r.success = true;
+        r.threshold = ps.t[node];
+        r.discarded = discarded;
+        r.budget_limit = p_max * e_budget;
+        r.finished_count = inactive;
+        r.fin_v = pr.est_sum[node];
+        launch_scan_counts(st, nblk, ws.cnt_multi.p + node * nblk, ws.off_probe.p);
+        return r;
+      }
+      const Dir dir = memory_ok ? kTowardMin : kTowardMax;
+      if (last != kNone && dir != last) {
+        ++r.direction_changes;
+        if (r.direction_changes > lim.direction_change_limit) {
+          t = ps.t[node];
+          done = true;
+          break;
+        }
+        const double stepped = p_max + lim.p_max_step;
+        p_max = (stepped < lim.p_max_cap) ? stepped : lim.p_max_cap;  // std::min(cap, p+step)
+      }
+      last = dir;
+      const int child = dir == kTowardMax ? 2 * node + 1 : 2 * node + 2;
+      t = child < kMaxProbes ? ps.t[child]
+                             : (dir == kTowardMax ? (ps.t[node] + max_err) * 0.5
+                                                  : (ps.t[node] + min_err) * 0.5);
+      if (r.attempts >= lim.attempt_limit) {
+        done = true;
+        break;
+      }
+      if (child >= kMaxProbes) break;  // next pass rooted at t
+      node = child;
     }
-    const Dir dir = memory_ok ? kTowardMin : kTowardMax;
-    if (last != kNone && dir != last) {
-      ++r.direction_changes;
-      if (r.direction_changes > lim.direction_change_limit) break;
-      const double stepped = p_max + lim.p_max_step;
-      p_max = (stepped < lim.p_max_cap) ? stepped : lim.p_max_cap;  // std::min(cap, p+step)
-    }
-    last = dir;
-    t = dir == kTowardMax ? (t + max_err) * 0.5 : (t + min_err) * 0.5;
   }
   r.threshold = t;
   r.budget_limit = p_max * e_budget;
@@ -418,6 +465,14 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     ep.len = ws.len[cur].p;
     ep.refine = (it > 1 && cfg.refiner == PAGANI_REFINER_TWO_LEVEL) ? 1 : 0;
     const size_t k0 = kt.mark();
+    const int64_t nblk = nblocks_of(m);
+    ep.nblk = nblk;
+    if (eval_k.fused_fold) {  // block folds + min/max run in k_evaluate's tail
+      ep.part = ws.part_eval.p;
+      ep.cnt = ws.cnt_eval.p;
+      ep.mm = ws.mm_blk.p;
+      ep.blk_done = ws.blk_done.p;
+    }
     launch_evaluate(eval_k, st, ep);
     PGN_CK(cudaGetLastError());
     const size_t k1 = kt.mark();
@@ -427,15 +482,16 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     out->region_evals += m;
 
     // ---- block folds: v, e, finished sums, active counts ---------------------
-    const int64_t nblk = nblocks_of(m);
-    launch_fold_eval(st, m, ws.est.p, ws.err.p, ws.flag.p, ws.part_eval.p, ws.cnt_eval.p);
+    if (!eval_k.fused_fold) {
+      launch_fold_eval(st, m, ws.est.p, ws.err.p, ws.flag.p, ws.part_eval.p, ws.cnt_eval.p);
+      out->kernel_launches[PAGANI_K_FOLD]++;
+    }
     const size_t k2 = kt.mark();
     launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
-                    ws.d_sc.p);
+                    ws.d_sc.p, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p);
     const size_t k3 = kt.mark();
     kt.span(PAGANI_K_FOLD, k1, k2);
     kt.span(PAGANI_K_FINALIZE, k2, k3);
-    out->kernel_launches[PAGANI_K_FOLD]++;
     out->kernel_launches[PAGANI_K_FINALIZE]++;
     PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
     PGN_CK(cudaStreamSynchronize(st));
@@ -490,14 +546,14 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     const int64_t* offsets = ws.off_eval.p;
     if (trig_digits || trig_memory) {
       double pms = 0.0;
-      const ThresholdOutcome tr =
-          device_threshold(ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf,
-                           acc_e + acc_ef, acc_e, m, cfg.tau_rel, lim, prof ? &pms : nullptr);
+      const double known_mm[2] = {sc.mn, sc.mx};
+      const ThresholdOutcome tr = device_threshold(
+          ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, m,
+          cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr);
       out->kernel_ms[PAGANI_K_PROBE] += pms;
-      out->kernel_launches[PAGANI_K_PROBE] += tr.attempts;
-      out->kernel_launches[PAGANI_K_FINALIZE] += tr.attempts;
+      out->kernel_launches[PAGANI_K_PROBE] += 2 * tr.passes + (tr.success ? 1 : 0);
       out->kernel_launches[PAGANI_K_MINMAX] += tr.minmax_launches;
-      out->d2h_bytes += tr.attempts * sizeof(FoldScalars);
+      out->d2h_bytes += tr.passes * sizeof(ProbeScalars);
       if (out->n_events < PAGANI_MAX_EVENTS) {
         pagani_threshold_event& ev = out->events[out->n_events];
         ev.iteration = it;

@@ -63,6 +63,12 @@ struct Workspace {
   DevBuf<uint8_t> axis, flag, flag2;
   DevBuf<double> part_eval, part_probe, scratch;
   DevBuf<int64_t> cnt_eval, cnt_probe, off_eval, off_probe;
+  DevBuf<int> blk_done;                 // fused-fold arrival counters (self-resetting)
+  DevBuf<unsigned long long> mm_blk;    // per-block min/max error keys
+  DevBuf<double> part_multi, scratch_multi;
+  DevBuf<int64_t> cnt_multi;
+  DevBuf<ProbeScalars> d_probe;
+  ProbeScalars* h_probe = nullptr;      // pinned
   DevBuf<FoldScalars> d_sc;
   DevBuf<unsigned long long> mm_keys;
   DevBuf<double> mm_out, d_lower, d_step, d_tmp;
@@ -91,6 +97,7 @@ struct ThresholdOutcome {
   int attempts = 0, direction_changes = 0;
   double fin_v = 0.0;  // sum of estimates where candidate == 0 (valid on success)
   int minmax_launches = 0;  // kernels launched by min_max (0 or 3)
+  int passes = 0;           // speculative probe passes (2 kernels + 1 D2H each)
 };
 
 struct Limits {
@@ -101,10 +108,12 @@ struct Limits {
 // classify.cpp:37-95 over device arrays (flags unchanged; candidates are
 // re-derived from the returned threshold).  Leaves, on success, the probe's
 // block offsets in ws.off_probe.
+// minmax: {min, max} of the errors if already known (fused fold), else null.
 ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
-                                  const Limits& lim, double* probe_ms);
+                                  const Limits& lim, double* probe_ms,
+                                  const double* minmax = nullptr);
 
 void integrate(const pagani_integrand* f, int ndim, const double* lower, const double* upper,
                const pagani_config* cfg, pagani_result* out);

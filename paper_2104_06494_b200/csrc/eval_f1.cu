@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f1(int mode) {
-  return {mode ? &k_evaluate_sep<N, F1, 1> : &k_evaluate_sep<N, F1, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F1, 1> : &k_evaluate_sep<N, F1, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f1(int n, int mode) {

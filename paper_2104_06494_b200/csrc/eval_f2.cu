@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f2(int mode) {
-  return {mode ? &k_evaluate_sep<N, F2, 1> : &k_evaluate_sep<N, F2, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F2, 1> : &k_evaluate_sep<N, F2, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f2(int n, int mode) {

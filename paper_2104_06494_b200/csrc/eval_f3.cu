@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f3(int mode) {
-  return {mode ? &k_evaluate_sep<N, F3, 1> : &k_evaluate_sep<N, F3, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F3, 1> : &k_evaluate_sep<N, F3, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f3(int n, int mode) {

@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f5(int mode) {
-  return {mode ? &k_evaluate_sep<N, F5, 1> : &k_evaluate_sep<N, F5, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F5, 1> : &k_evaluate_sep<N, F5, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f5(int n, int mode) {

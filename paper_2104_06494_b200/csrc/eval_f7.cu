@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f7(int mode) {
-  return {mode ? &k_evaluate_sep<N, F7, 1> : &k_evaluate_sep<N, F7, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F7, 1> : &k_evaluate_sep<N, F7, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f7(int n, int mode) {

@@ -6,7 +6,7 @@ namespace pgn {
 
 template <int N>
 static EvalLaunch pick_f8(int mode) {
-  return {mode ? &k_evaluate_sep<N, F8, 1> : &k_evaluate_sep<N, F8, 0>, eval_smem_bytes<N>()};
+  return {mode ? &k_evaluate_sep<N, F8, 1> : &k_evaluate_sep<N, F8, 0>, eval_smem_bytes<N>(), true};
 }
 
 EvalLaunch lookup_eval_f8(int n, int mode) {

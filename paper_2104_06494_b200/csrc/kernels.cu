@@ -161,6 +161,100 @@ __global__ void __launch_bounds__(kFoldThreads)
   part[(threadIdx.x == 0 ? 0 : 1) * nblk + b] = fin;
 }
 
+// Speculative threshold probes: T <= kMaxProbes candidate thresholds (a
+// level-order tree of the search's possible next steps, classify.cpp:82-89)
+// evaluated in ONE pass.  The block is staged in smem once; lane i of warp 0
+// folds err where cand_i == 0 and counts cand_i == 1, lane i of warp 1 folds
+// est where cand_i == 0 -- T serial chains in the latency of one.
+__global__ void __launch_bounds__(kFoldThreads)
+    k_probe_multi(int64_t m, int64_t nblk, ProbeSet ts, const double* __restrict__ est,
+                  const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
+                  int64_t* cnt) {
+  __shared__ FoldSmem S;
+  const int64_t b = blockIdx.x;
+  const int64_t lo = b * kBlock;
+  const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
+  stage_block(S, est, err, flag, lo, n, true, 0.0, false);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w > 1 || lane >= ts.T) return;
+  const double t = ts.t[lane];
+  const double* x = w == 0 ? S.err : S.est;
+  double fin = 0.0;
+  int64_t c = 0;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) {
+    const bool c1 = S.flag[i] && !(S.err[i] < t);
+    c += c1;
+    fin = P_ADD(fin, c1 ? 0.0 : x[i]);
+  }
+  part[(w * kMaxProbes + lane) * nblk + b] = fin;
+  if (w == 0) cnt[lane * nblk + b] = c;
+}
+
+// Pairwise trees (reduce.cpp:13-27) for 2T fold arrays + T count totals:
+// one CTA per array.
+__global__ void __launch_bounds__(256)
+    k_finalize_multi(int64_t nblk, int T, const double* part, const int64_t* cnt, double* scratch,
+                     ProbeScalars* out) {
+  const int id = blockIdx.x;  // 0..2T-1 folds, 2T..3T-1 counts
+  const int tid = threadIdx.x;
+  if (id >= 2 * T) {
+    __shared__ long long s_c[256];
+    const int i = id - 2 * T;
+    long long c = 0;
+    for (int64_t k = tid; k < nblk; k += 256) c += cnt[i * nblk + k];
+    s_c[tid] = c;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (tid < o) s_c[tid] += s_c[tid + o];
+      __syncthreads();
+    }
+    if (tid == 0) out->count[i] = s_c[0];
+    return;
+  }
+  const int w = id / T, i = id % T;
+  const double* src = part + (w * kMaxProbes + i) * nblk;
+  double* bufs[2] = {scratch + static_cast<int64_t>(id) * 2 * nblk,
+                     scratch + static_cast<int64_t>(id) * 2 * nblk + nblk};
+  int cur_buf = 0;
+  int64_t cur = nblk;
+  while (cur > 1) {
+    const int64_t half = cur / 2;
+    double* dst = bufs[cur_buf];
+    for (int64_t k = tid; k < half; k += 256) dst[k] = P_ADD(src[2 * k], src[2 * k + 1]);
+    if ((cur & 1) && tid == 0) dst[half] = src[cur - 1];
+    __syncthreads();
+    src = dst;
+    cur_buf ^= 1;
+    cur = half + (cur & 1);
+  }
+  if (tid == 0) (w == 0 ? out->err_sum : out->est_sum)[i] = nblk ? src[0] : 0.0;
+}
+
+// Exclusive scan of one count row (offsets of the accepted probe).
+__global__ void __launch_bounds__(1024) k_scan_counts(int64_t nblk, const int64_t* cnt,
+                                                      int64_t* offsets) {
+  __shared__ int64_t s_sum[1024];
+  const int tid = threadIdx.x;
+  const int64_t chunk = (nblk + 1023) / 1024;
+  const int64_t lo = tid * chunk, hi = lo + chunk < nblk ? lo + chunk : nblk;
+  int64_t local = 0;
+  for (int64_t i = lo; i < hi; ++i) local += cnt[i];
+  s_sum[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int64_t v = tid >= off ? s_sum[tid - off] : 0;
+    __syncthreads();
+    s_sum[tid] += v;
+    __syncthreads();
+  }
+  int64_t run = s_sum[tid] - local;
+  for (int64_t i = lo; i < hi; ++i) {
+    offsets[i] = run;
+    run += cnt[i];
+  }
+}
+
 __global__ void k_candidates(int64_t m, double t, const uint8_t* flag, const double* err,
                              uint8_t* out) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -185,9 +279,43 @@ constexpr int kFinThreads = 1024;
 
 __global__ void __launch_bounds__(kFinThreads)
     k_finalize(int64_t nblk, int nq, const double* part, const int64_t* cnt, int64_t* offsets,
-               double* scratch, FoldScalars* out) {
+               double* scratch, FoldScalars* out, const unsigned long long* mm,
+               const double* err0) {
   __shared__ int64_t s_sum[kFinThreads];
+  __shared__ unsigned long long s_k[2][kFinThreads / 32];
   const int tid = threadIdx.x;
+  if (mm) {  // min_max of the errors from per-block keys (reduce.cpp:74-82; exact)
+    unsigned long long a = ~0ULL, z = 0ULL;
+    for (int64_t i = tid; i < nblk; i += kFinThreads) {
+      a = mm[2 * i] < a ? mm[2 * i] : a;
+      z = mm[2 * i + 1] > z ? mm[2 * i + 1] : z;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, a, o);
+      const unsigned long long z2 = __shfl_xor_sync(0xffffffffu, z, o);
+      a = a2 < a ? a2 : a;
+      z = z2 > z ? z2 : z;
+    }
+    if ((tid & 31) == 0) {
+      s_k[0][tid >> 5] = a;
+      s_k[1][tid >> 5] = z;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < kFinThreads / 32; ++q) {
+        a = s_k[0][q] < a ? s_k[0][q] : a;
+        z = s_k[1][q] > z ? s_k[1][q] : z;
+      }
+      const double x0 = err0[0];
+      if (x0 != x0) {  // both start at x[0]; a NaN there sticks
+        out->mn = x0;
+        out->mx = x0;
+      } else {
+        out->mn = key_val(a);
+        out->mx = key_val(z);
+      }
+    }
+  }
   // reduce.cpp:13-27: p[i] = p[2i] + p[2i+1] level by level, odd tail carried.
   for (int q = 0; q < nq; ++q) {
     const double* src = part + q * nblk;
@@ -234,14 +362,6 @@ __global__ void __launch_bounds__(kFinThreads)
 }
 
 // ---- min / max ---------------------------------------------------------------
-__device__ __forceinline__ unsigned long long ord_key(double v) {
-  const unsigned long long b = pgn_asu64(v);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
-}
-__device__ __forceinline__ double key_val(unsigned long long k) {
-  return pgn_asf64((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k);
-}
-
 __global__ void k_minmax_init(unsigned long long* keys) {
   keys[0] = ~0ULL;
   keys[1] = 0ULL;
@@ -481,6 +601,20 @@ void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const
                                                                  cnt);
 }
 
+void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
+                        const double* err, const uint8_t* flag, double* part, int64_t* cnt,
+                        double* scratch, ProbeScalars* out) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_probe_multi<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, ts, est, err, flag,
+                                                                       part, cnt);
+  k_finalize_multi<<<3 * ts.T, 256, 0, st>>>(nblk, ts.T, part, cnt, scratch, out);
+}
+
+void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets) {
+  if (nblk > 0) k_scan_counts<<<1, 1024, 0, st>>>(nblk, cnt, offsets);
+}
+
 void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,
                        const double* err, uint8_t* out) {
   if (m > 0) k_candidates<<<grid_for(m, 256), 256, 0, st>>>(m, t, flag, err, out);
@@ -494,8 +628,9 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 }
 
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
-                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out) {
-  k_finalize<<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out);
+                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
+                     const unsigned long long* mm, const double* err0) {
+  k_finalize<<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm, err0);
 }
 
 void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,

@@ -22,12 +22,27 @@ struct FoldScalars {
   double sum[4];
   int64_t count;
   int64_t pad;
+  double mn, mx;  // min/max of the errors (when block keys are supplied)
+};
+
+// Speculative probe set: a level-order binary tree of candidate thresholds.
+constexpr int kMaxProbes = 15;
+struct ProbeSet {
+  int T;
+  int pad;
+  double t[kMaxProbes];
+};
+struct ProbeScalars {
+  double err_sum[kMaxProbes];  // sum err where candidate == 0 (discarded)
+  double est_sum[kMaxProbes];  // sum est where candidate == 0
+  long long count[kMaxProbes]; // #candidate == 1
 };
 
 using EvalKernel = void (*)(const EvalParams, const uint64_t*, const double*);
 struct EvalLaunch {
   EvalKernel fn = nullptr;
-  size_t smem = 0;  // dynamic shared memory bytes
+  size_t smem = 0;          // dynamic shared memory bytes
+  bool fused_fold = false;  // kernel runs the 2048-block folds in its tail
 };
 
 // ---- launchers (kernels.cu) ------------------------------------------------
@@ -52,9 +67,18 @@ void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag
 void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t* flag,
                      int which, double* part, int64_t* cnt);
 
-// Pairwise trees over nq partial arrays (stride nblk) + exclusive scan of cnt.
+// Pairwise trees over nq partial arrays (stride nblk) + exclusive scan of cnt
+// (+ min/max of the errors from per-block keys mm, if given; err0 = &err[0]).
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
-                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out);
+                     const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
+                     const unsigned long long* mm = nullptr, const double* err0 = nullptr);
+
+// T speculative probes in one pass + their trees; part [2][kMaxProbes][nblk],
+// cnt [kMaxProbes][nblk], scratch 2*3*kMaxProbes*nblk doubles.
+void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
+                        const double* err, const uint8_t* flag, double* part, int64_t* cnt,
+                        double* scratch, ProbeScalars* out);
+void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets);
 
 // min_max over err (reduce.cpp:74-82).  out[0] = min, out[1] = max, as doubles.
 void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,
