@@ -19,8 +19,8 @@ max_regions=2^22 (the reference defaults), relative filtering off for f1 only
           host cores on a bounded sample of the same workload
 
 --impl reference runs that reference library (all host threads) on the
-bounded sample for every step.  Multi-GPU (torchrun): each rank runs the
-workload on its own GPU (weak scaling, "replicas") -- see DESIGN.md.
+bounded sample for every step.  Multi-GPU (torchrun): the region list of every
+integrate() is sharded over the ranks (NCCL; strong scaling) -- DESIGN.md §7.
 """
 from __future__ import annotations
 
@@ -118,11 +118,25 @@ def run_ours(args, rank, world, local_rank):
     from paper_2104_06494_b200 import roofline
 
     torch = None
+    comm = None
+    parallelism = "1 GPU"
     if world > 1:
         import torch
         import torch.distributed as dist
+        local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # gloo host transport: lets several ranks share one GPU (testing)
+            dist.init_process_group("gloo")
+        from paper_2104_06494_b200 import dist as pdist
+        try:  # sharded: one region list split over the ranks (strong scaling)
+            comm = pdist.from_torch(local_rank)
+            parallelism = (f"sharded over {world} ranks ({args.dist_backend}: allgather of block "
+                           f"records + send/recv exchange, DESIGN.md 7)")
+        except Exception as e:  # noqa: BLE001 - still GPU work, just not sharded
+            comm = None
+            parallelism = f"replicas x{world} (sharding unavailable: {e})"
     device = local_rank
 
     def barrier_sync():
@@ -130,19 +144,19 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
             torch.cuda.synchronize()
 
-    def max_over_ranks(x):
+    def _reduce(x, op):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev = "cuda" if args.dist_backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=op)
         return float(t.item())
 
+    def max_over_ranks(x):
+        return _reduce(x, torch.distributed.ReduceOp.MAX) if world > 1 else x
+
     def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
-        return float(t.item())
+        return _reduce(x, torch.distributed.ReduceOp.SUM) if world > 1 else x
 
     mode = args.mode
     cases = workload(args.cases)
@@ -151,7 +165,7 @@ def run_ours(args, rank, world, local_rank):
         rs = []
         for fid, tau in cases:
             cfg = pg.Config(tau_rel=tau, rel_filtering_enabled=(fid != 1), max_regions=args.max_regions,
-                            mode=mode, device=device, profile=profile)
+                            mode=mode, device=device, profile=profile, comm=comm)
             rs.append((fid, tau, pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(DIM), cfg)))
         return rs
 
@@ -210,13 +224,14 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_s_max * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if comm is not None or world == 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's fixed-parameter Genz integrands (deterministic, no dataset)",
         "config": {"workload": "genz_8d_suite: f1..f6 x tau in {1e-3,1e-4,1e-5,1e-6}, n=8, "
                                "tau_abs=1e-20, it_max=100, rel filter off for f1",
                    "max_regions": args.max_regions, "mode": mode,
                    "l2": "working set > L2: each run streams a region store of up to 1.1 GB",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": parallelism},
         "roofline": {"bound": "fp64", "kernel": "k_evaluate_sep", "achieved": achieved,
                      "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / peak_tflops if peak_tflops else None,
@@ -306,6 +321,8 @@ def main():
     ap.add_argument("--mode", default="parity", choices=["parity", "fast"])
     ap.add_argument("--max-regions", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = host transport, for running several ranks on one GPU")
     ap.add_argument("--cases", default=None,
                     help="profiling subset, e.g. f4@1e-3 (the default is the whole suite)")
     args = ap.parse_args()

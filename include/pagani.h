@@ -256,9 +256,10 @@ int pagani_check_termination(double v, double e, double v_f, double e_f, double 
 int pagani_digits_converged(double v_prev, double v_curr, int digits);
 int pagani_convergence_digits(double tau_rel);
 
-/* glibc-exact math used by the device integrands, exported for verification
- * (evaluates on the GPU when on_device != 0, else the host build of the same
- * source). */
+/* glibc-exact math used by the device integrands, exported for verification.
+ * exp: on_device 0 = host build of the same source, 1 = GPU.
+ * cos: 0 = host gm_cos, 1 = GPU gm_cos, 2 = GPU branch-free gm_cos_bf (used by
+ * f1), 3 = host gm_cos_bf. */
 int pagani_math_exp(int64_t m, const double* x, double* y, int32_t on_device);
 int pagani_math_cos(int64_t m, const double* x, double* y, int32_t on_device);
 /* Evaluate a builtin integrand at host points (m x n), on the device. */
@@ -278,7 +279,31 @@ int pagani_fp64_peak(int device, double seconds, double* tflops, double* sm_mhz)
 int pagani_comm_unique_id(uint8_t* unique_id);
 int pagani_comm_init_rank(const uint8_t* unique_id, int nranks, int rank, int device,
                           void** comm);
+/* Host-callback transport (e.g. torch.distributed / gloo): the library stages
+ * device buffers through host memory and calls back.  Lets R ranks share one
+ * GPU (tests) or run where NCCL is unavailable.  Callbacks return 0 on success.
+ *   allgather: recv holds size * bytes, rank-major.
+ *   exchange : one group of point-to-point sends and receives. */
+typedef struct pagani_host_transport {
+  int32_t rank, size;
+  void* user;
+  int (*allgather)(const void* send, void* recv, size_t bytes, void* user);
+  int (*exchange)(int n_send, const int* send_peer, const void* const* send_buf,
+                  const size_t* send_bytes, int n_recv, const int* recv_peer,
+                  void* const* recv_buf, const size_t* recv_bytes, void* user);
+} pagani_host_transport;
+int pagani_comm_init_host(const pagani_host_transport* transport, int device, void** comm);
 int pagani_comm_destroy(void* comm);
+
+/* Shard logic (host only; exported so it can be tested without a GPU).
+ * pagani_shard_bounds: balanced 2048-block-aligned partition of m regions,
+ * nranks+1 boundaries.  pagani_shard_plan: given kept[r] (global kept index of
+ * rank r's first kept region, nranks+1 entries), the pieces rank `rank` sends
+ * and receives when the 2*kept[nranks] children are re-partitioned; each piece
+ * is 4 int64 {peer, src_offset, dst_offset, count}. */
+int pagani_shard_bounds(int64_t m, int nranks, int64_t* bounds);
+int pagani_shard_plan(int nranks, int rank, const int64_t* kept, int max_pieces, int32_t* n_send,
+                      int64_t* sends, int32_t* n_recv, int64_t* recvs);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -100,6 +100,19 @@ class ThresholdResult(C.Structure):
                 ("budget_limit", C.c_double), ("finished_count", C.c_int64)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p),
+                          C.POINTER(C.c_size_t), C.c_int, C.POINTER(C.c_int),
+                          C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_void_p)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("user", C.c_void_p),
+                ("allgather", ALLGATHER_FN), ("exchange", EXCHANGE_FN)]
+
+
+PAGANI_COMM_ID_BYTES = 128
+
 _D = C.POINTER(C.c_double)
 _U8 = C.POINTER(C.c_uint8)
 _I32 = C.POINTER(C.c_int32)
@@ -147,7 +160,12 @@ SIGNATURES = {
     "pagani_comm_unique_id": (C.c_int, [_U8]),
     "pagani_comm_init_rank": (C.c_int, [_U8, C.c_int, C.c_int, C.c_int,
                                         C.POINTER(C.c_void_p)]),
+    "pagani_comm_init_host": (C.c_int, [C.POINTER(HostTransport), C.c_int,
+                                        C.POINTER(C.c_void_p)]),
     "pagani_comm_destroy": (C.c_int, [C.c_void_p]),
+    "pagani_shard_bounds": (C.c_int, [C.c_int64, C.c_int, _I64]),
+    "pagani_shard_plan": (C.c_int, [C.c_int, C.c_int, _I64, C.c_int, C.POINTER(C.c_int32), _I64,
+                                    C.POINTER(C.c_int32), _I64]),
 }
 
 _lib = None

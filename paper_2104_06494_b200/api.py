@@ -124,6 +124,7 @@ class Config:
     mode: str = "parity"  # "parity" (bit-exact) | "fast"
     device: int = 0
     profile: bool = False
+    comm: object = None  # dist.Communicator for multi-GPU runs (one process per GPU)
 
     def convergence_digits(self) -> int:  # driver.cpp:28-33
         return _lib().pagani_convergence_digits(self.tau_rel)
@@ -154,6 +155,7 @@ class Config:
         c.mode = {"parity": N.MODE_PARITY, "fast": N.MODE_FAST}[self.mode]
         c.device = self.device
         c.profile = int(bool(self.profile))
+        c.comm = self.comm.handle if self.comm is not None else None
         return c
 
 
@@ -560,10 +562,12 @@ def glibc_exp(x, on_device=True):
     return y
 
 
-def glibc_cos(x, on_device=True):
+def glibc_cos(x, on_device=True, branch_free=False):
+    """glibc cos restatement; branch_free selects the SIMT variant used by f1."""
     x = _f64(x)
     y = np.empty_like(x)
-    N.check(_lib().pagani_math_cos(len(x), _dp(x), _dp(y), int(on_device)))
+    code = (2 if on_device else 3) if branch_free else int(bool(on_device))
+    N.check(_lib().pagani_math_cos(len(x), _dp(x), _dp(y), code))
     return y
 
 

@@ -8,8 +8,12 @@
 #include "driver.hpp"
 
 namespace {
-
 thread_local std::string g_last_error;
+}  // namespace
+
+void pgn::set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
 
 template <class Fn>
 int guarded(Fn&& fn) {
@@ -19,6 +23,9 @@ int guarded(Fn&& fn) {
   } catch (const pgn::CudaError& e) {
     g_last_error = e.what();
     return PAGANI_E_CUDA;
+  } catch (const pgn::NcclError& e) {
+    g_last_error = e.what();
+    return PAGANI_E_NCCL;
   } catch (const pgn::UnsupportedError& e) {
     g_last_error = e.what();
     return PAGANI_E_UNSUPPORTED;
@@ -505,17 +512,21 @@ int pagani_math_exp(int64_t m, const double* x, double* y, int32_t on_device) {
 }
 
 int pagani_math_cos(int64_t m, const double* x, double* y, int32_t on_device) {
+  // on_device: 0 host build, 1 device gm_cos, 2 device branch-free gm_cos_bf,
+  // 3 host build of gm_cos_bf
   return guarded([&] {
-    if (!on_device) {
+    if (on_device == 0 || on_device == 3) {
       static const uint64_t SC[] = PGN_SINCOS_TAB_INIT;
-      for (int64_t i = 0; i < m; ++i) y[i] = pgn::gm_cos(x[i], reinterpret_cast<const double*>(SC));
+      const double* sc = reinterpret_cast<const double*>(SC);
+      for (int64_t i = 0; i < m; ++i)
+        y[i] = on_device ? pgn::gm_cos_bf(x[i], sc) : pgn::gm_cos(x[i], sc);
       return;
     }
     if (m <= 0) return;
     Ctx c;
     pgn::DevBuf<double> dx, dy(m);
     h2d(dx, x, m, c.st);
-    pgn::launch_math(c.st, 1, m, dx.p, dy.p);
+    pgn::launch_math(c.st, on_device == 2 ? 2 : 1, m, dx.p, dy.p);
     d2h(y, dy.p, m, c.st);
     PGN_CK(cudaStreamSynchronize(c.st));
   });

@@ -94,7 +94,53 @@ Workspace::~Workspace() {
   if (h_sc) cudaFreeHost(h_sc);
   if (h_mm) cudaFreeHost(h_mm);
   if (h_probe) cudaFreeHost(h_probe);
+  if (h_kb) cudaFreeHost(h_kb);
   if (st) cudaStreamDestroy(st);
+}
+
+void Workspace::ensure_shard(int R, int n_, int64_t nb_global, int64_t nblk_max_cap,
+                             int64_t stage) {
+  stage = ((stage + kBlock - 1) / kBlock) * kBlock;
+  if (nb_global <= nb_global_cap && stage <= stage_cap && n_ <= stage_n &&
+      rec_send.n >= static_cast<size_t>(nblk_max_cap + 1) &&
+      rec_recv.n >= static_cast<size_t>(R) * (nblk_max_cap + 1))
+    return;
+  PGN_CK(cudaSetDevice(device));
+  nb_global_cap = nb_global > nb_global_cap ? nb_global : nb_global_cap;
+  stage_cap = stage > stage_cap ? stage : stage_cap;
+  const int64_t nb = nb_global_cap;
+  g_part.alloc(4 * nb);
+  g_err0.alloc(1);
+  g_cnt.alloc(nb);
+  g_off.alloc(nb);
+  g_off_probe.alloc(nb);
+  g_mm.alloc(2 * nb);
+  g_part_multi.alloc(2 * kMaxProbes * nb);
+  g_cnt_multi.alloc(kMaxProbes * nb);
+  g_scratch_multi.alloc(2 * 2 * kMaxProbes * nb + 2);
+  g_scratch.alloc(2 * nb + 2);
+  g_kb.alloc(kMaxRanks + 1);
+  rec_send.alloc(nblk_max_cap + 1);
+  rec_recv.alloc(static_cast<size_t>(R) * (nblk_max_cap + 1));
+  prec_send.alloc(nblk_max_cap + 1);
+  prec_recv.alloc(static_cast<size_t>(R) * (nblk_max_cap + 1));
+  const int nn = n_ > stage_n ? n_ : stage_n;
+  stage_n = nn;
+  st_low.alloc(static_cast<size_t>(nn) * stage_cap);
+  st_len.alloc(static_cast<size_t>(nn) * stage_cap);
+  st_pest.alloc(stage_cap);
+  if (!h_kb) PGN_CK(cudaMallocHost(&h_kb, (kMaxRanks + 1) * sizeof(int64_t)));
+}
+
+void ShardCtx::set_bounds(std::vector<int64_t> b) {
+  bounds = std::move(b);
+  rb.R = R;
+  nblk_max = max_blocks(bounds);
+  nblk_global = nblocks_of(bounds[R]);
+  for (int r = 0; r < R; ++r) {
+    rb.first[r] = bounds[r] / kBlock;
+    rb.nblk[r] = nblocks_of(bounds[r + 1] - bounds[r]);
+  }
 }
 
 namespace {
@@ -192,7 +238,8 @@ int initial_subdivisions(int n, int64_t init_target) {  // geometry.cpp:67-81
 ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
-                                  const Limits& lim, double* probe_ms, const double* minmax) {
+                                  const Limits& lim, double* probe_ms, const double* minmax,
+                                  ShardCtx* sh) {
   ThresholdOutcome r;
   if (s_it <= 0) return r;
   const double e_budget = e_tot - std::fabs(v_tot) * tau_rel;
@@ -235,8 +282,19 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
     }
     cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
     if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
-    launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
-                       ws.scratch_multi.p, ws.d_probe.p);
+    if (!sh) {
+      launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
+                         ws.scratch_multi.p, ws.d_probe.p);
+    } else {  // local blocks -> allgather of block records -> global trees on every rank
+      launch_probe_only(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p);
+      launch_pack_probe(st, nblocks_of(m), sh->nblk_max, kMaxProbes, ws.part_multi.p,
+                        ws.cnt_multi.p, ws.prec_send.p);
+      sh->comm->allgather(ws.prec_send.p, ws.prec_recv.p, sh->nblk_max * sizeof(ProbeRec), st);
+      launch_unpack_probe(st, sh->rb, sh->nblk_max, sh->nblk_global, kMaxProbes, ws.prec_recv.p,
+                          ws.g_part_multi.p, ws.g_cnt_multi.p);
+      launch_finalize_multi(st, sh->nblk_global, kMaxProbes, ws.g_part_multi.p, ws.g_cnt_multi.p,
+                            ws.g_scratch_multi.p, ws.d_probe.p);
+    }
     if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
     PGN_CK(cudaMemcpyAsync(ws.h_probe, ws.d_probe.p, sizeof(ProbeScalars), cudaMemcpyDeviceToHost,
                            st));
@@ -261,7 +319,15 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
         r.budget_limit = p_max * e_budget;
         r.finished_count = inactive;
         r.fin_v = pr.est_sum[node];
-        launch_scan_counts(st, nblk, ws.cnt_multi.p + node * nblk, ws.off_probe.p);
+        r.node = node;
+        if (!sh) {
+          launch_scan_counts(st, nblk, ws.cnt_multi.p + node * nblk, ws.off_probe.p);
+        } else {
+          const int64_t ng = sh->nblk_global;
+          launch_scan_counts(st, ng, ws.g_cnt_multi.p + node * ng, ws.g_off_probe.p);
+          launch_gather_bounds(st, sh->rb, ws.g_off_probe.p, ws.g_cnt_multi.p + node * ng, ng,
+                               ws.g_kb.p);
+        }
         return r;
       }
       const Dir dir = memory_ok ? kTowardMin : kTowardMax;
@@ -365,10 +431,29 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     throw std::invalid_argument("Config: unknown mode");
   const EvalLaunch eval_k = lookup_evaluate(di.fid, n, cfg.mode);
   if (!eval_k.fn) throw UnsupportedError("no device kernel for this integrand/dimension");
-  if (cfg.comm) throw UnsupportedError("multi-GPU communicator passed to the 1-GPU driver");
+
+  // ---- ranks ------------------------------------------------------------------
+  Comm* comm = comm_from_handle(cfg.comm);
+  const int R = comm ? comm->size() : 1;
+  ShardCtx shard;
+  ShardCtx* sh = nullptr;
+  // A communicator always selects the sharded path (R = 1 included: this is
+  // how the NCCL transport is exercised on a single-GPU host).
+  if (comm) {
+    if (R > kMaxRanks) throw std::invalid_argument("too many ranks");
+    if (!eval_k.fused_fold)
+      throw UnsupportedError("multi-GPU runs need a builtin separable integrand (f1..f8)");
+    if (cfg.validate_invariants)
+      throw UnsupportedError("validate_invariants is single-GPU only");
+    shard.comm = comm;
+    shard.R = R;
+    shard.rank = comm->rank();
+    sh = &shard;
+  }
+  const int rank = sh ? sh->rank : 0;
 
   std::memset(out, 0, sizeof(*out));
-  Workspace& ws = workspace_for(cfg.device);
+  Workspace& ws = workspace_for(comm ? comm->device() : cfg.device);
   std::lock_guard<std::mutex> lock(ws.mu);
   PGN_CK(cudaSetDevice(ws.device));
   cudaStream_t st = ws.st;
@@ -386,21 +471,34 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
   const RuleOrbits rule = build_rule_orbits(n);  // rule.cpp:166
   const int d = cfg.init_subdiv > 0 ? cfg.init_subdiv : initial_subdivisions(n, cfg.init_target);
-  int64_t m = 1;  // geometry.cpp:86-94
+  int64_t M = 1;  // global batch size (geometry.cpp:86-94)
   for (int a = 0; a < n; ++a) {
-    if (m > cfg.max_regions / d) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
-    m *= d;
+    if (M > cfg.max_regions / d) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
+    M *= d;
   }
-  if (m > cfg.max_regions) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
+  if (M > cfg.max_regions) throw std::runtime_error("uniform_split: d^n exceeds max_regions");
 
-  ws.ensure(n, cfg.max_regions > m ? cfg.max_regions : m);
+  // capacity: the whole cap on one GPU; a balanced block share (+ the staging
+  // of this rank's children) when sharded
+  const int64_t glob_cap = cfg.max_regions > M ? cfg.max_regions : M;
+  int64_t cap_local = glob_cap;
+  if (sh) {
+    const int64_t nbg = nblocks_of(glob_cap);
+    cap_local = ((nbg + R - 1) / R) * kBlock;
+    sh->set_bounds(shard_bounds(M, R));
+    ws.ensure(n, cap_local);
+    ws.ensure_shard(R, n, nbg + 1, (nbg + R - 1) / R + 1, 2 * ws.cap);
+  } else {
+    ws.ensure(n, cap_local);
+  }
   const int64_t cap = ws.cap;
+  int64_t m = sh ? sh->local() : M;  // local batch size
   const bool prof = cfg.profile != 0;
   KTimer kt(ws, prof);
   cudaEvent_t ev_begin = ws.event(kSpanBegin), ev_end = ws.event(kSpanEnd);
   PGN_CK(cudaEventRecord(ev_begin, st));
 
-  {  // uniform split of the unit cube
+  {  // uniform split of the unit cube (this rank's slice of it)
     double lo[kMaxDim], step[kMaxDim];
     for (int a = 0; a < n; ++a) {
       lo[a] = 0.0;
@@ -409,7 +507,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     PGN_CK(cudaMemcpyAsync(ws.d_lower.p, lo, n * sizeof(double), cudaMemcpyHostToDevice, st));
     PGN_CK(cudaMemcpyAsync(ws.d_step.p, step, n * sizeof(double), cudaMemcpyHostToDevice, st));
     const size_t a0 = kt.mark();
-    launch_uniform_split(st, n, d, m, cap, ws.low[0].p, ws.len[0].p, ws.d_lower.p, ws.d_step.p);
+    launch_uniform_split(st, n, d, m, cap, ws.low[0].p, ws.len[0].p, ws.d_lower.p, ws.d_step.p,
+                         sh ? sh->first() : 0);
     kt.span(PAGANI_K_INIT, a0, kt.mark());
     out->kernel_launches[PAGANI_K_INIT]++;
     out->h2d_bytes += 2 * n * sizeof(double);
@@ -445,10 +544,11 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   double acc_v = 0.0, acc_e = 0.0, acc_vf = 0.0, acc_ef = 0.0;  // Accumulators
   double prev_total = std::numeric_limits<double>::quiet_NaN();
   const int digits = convergence_digits(cfg.tau_rel);
-  out->regions_generated = m;
+  out->regions_generated = M;
   out->peak_regions = m;
   int cur = 0;  // which low/len buffer holds the batch
   double finished_volume = 0.0;
+  std::vector<int64_t> kb(R + 1, 0);  // global kept offsets at rank boundaries
 
   auto finish = [&](int status, int it) {
     out->status = status;
@@ -459,7 +559,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
   bool done = false;
   for (int it = 1; it <= cfg.it_max && !done; ++it) {
-    // ---- evaluate (+ refine + classify) -------------------------------------
+    // ---- evaluate (+ refine + classify + block folds) -------------------------
     ep.m = m;
     ep.low = ws.low[cur].p;
     ep.len = ws.len[cur].p;
@@ -473,36 +573,56 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       ep.mm = ws.mm_blk.p;
       ep.blk_done = ws.blk_done.p;
     }
-    launch_evaluate(eval_k, st, ep);
-    PGN_CK(cudaGetLastError());
+    if (m > 0) {
+      launch_evaluate(eval_k, st, ep);
+      PGN_CK(cudaGetLastError());
+    }
     const size_t k1 = kt.mark();
     kt.span(PAGANI_K_EVALUATE, k0, k1);
-    out->kernel_launches[PAGANI_K_EVALUATE]++;
-    out->eval_count += m * rule.point_count;
+    out->kernel_launches[PAGANI_K_EVALUATE] += m > 0;
+    out->eval_count += M * rule.point_count;
     out->region_evals += m;
 
-    // ---- block folds: v, e, finished sums, active counts ---------------------
+    // ---- global scalars: v, e, finished sums, active counts, min/max ----------
     if (!eval_k.fused_fold) {
       launch_fold_eval(st, m, ws.est.p, ws.err.p, ws.flag.p, ws.part_eval.p, ws.cnt_eval.p);
       out->kernel_launches[PAGANI_K_FOLD]++;
     }
     const size_t k2 = kt.mark();
-    launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
-                    ws.d_sc.p, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p);
+    const int64_t* offsets = ws.off_eval.p;  // kept offsets, indexed by (global) block
+    if (!sh) {
+      launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
+                      ws.d_sc.p, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p);
+      out->kernel_launches[PAGANI_K_FINALIZE]++;
+    } else {  // allgather the block records; every rank runs the same global trees
+      launch_pack_blocks(st, nblk, sh->nblk_max, ws.part_eval.p, ws.cnt_eval.p, ws.mm_blk.p,
+                         ws.err.p, ws.rec_send.p);
+      comm->allgather(ws.rec_send.p, ws.rec_recv.p, (sh->nblk_max + 1) * sizeof(BlockRec), st);
+      launch_unpack_blocks(st, sh->rb, sh->nblk_max, sh->nblk_global, ws.rec_recv.p, ws.g_part.p,
+                           ws.g_cnt.p, ws.g_mm.p, ws.g_err0.p);
+      launch_finalize(st, sh->nblk_global, 4, ws.g_part.p, ws.g_cnt.p, ws.g_off.p, ws.g_scratch.p,
+                      ws.d_sc.p, ws.g_mm.p, ws.g_err0.p);
+      launch_gather_bounds(st, sh->rb, ws.g_off.p, ws.g_cnt.p, sh->nblk_global, ws.g_kb.p);
+      PGN_CK(cudaMemcpyAsync(ws.h_kb, ws.g_kb.p, (R + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             st));
+      out->kernel_launches[PAGANI_K_FINALIZE] += 4;
+      offsets = ws.g_off.p;
+    }
     const size_t k3 = kt.mark();
     kt.span(PAGANI_K_FOLD, k1, k2);
     kt.span(PAGANI_K_FINALIZE, k2, k3);
-    out->kernel_launches[PAGANI_K_FINALIZE]++;
     PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
     PGN_CK(cudaStreamSynchronize(st));
     out->d2h_bytes += sizeof(FoldScalars);
+    if (sh)
+      for (int r = 0; r <= R; ++r) kb[r] = ws.h_kb[r];
     const FoldScalars sc = ws.h_sc[0];
     acc_v = sc.sum[0];  // block_sum(estimates)
     acc_e = sc.sum[1];  // block_sum(errors)
 
     pagani_trace_row row{};
     row.it = it;
-    row.m = m;
+    row.m = M;
     row.active_rel = sc.count;
 
     if (cfg.validate_invariants) {  // driver.cpp:75-79,148
@@ -543,22 +663,21 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     double t_accepted = 0.0;
     double fin_v = sc.sum[2], fin_e = sc.sum[3];
     int64_t kept = sc.count;
-    const int64_t* offsets = ws.off_eval.p;
     if (trig_digits || trig_memory) {
       double pms = 0.0;
       const double known_mm[2] = {sc.mn, sc.mx};
       const ThresholdOutcome tr = device_threshold(
-          ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, m,
-          cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr);
+          ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, M,
+          cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr, sh);
       out->kernel_ms[PAGANI_K_PROBE] += pms;
-      out->kernel_launches[PAGANI_K_PROBE] += 2 * tr.passes + (tr.success ? 1 : 0);
+      out->kernel_launches[PAGANI_K_PROBE] += (sh ? 5 : 2) * tr.passes + (tr.success ? 1 : 0);
       out->kernel_launches[PAGANI_K_MINMAX] += tr.minmax_launches;
       out->d2h_bytes += tr.passes * sizeof(ProbeScalars);
       if (out->n_events < PAGANI_MAX_EVENTS) {
         pagani_threshold_event& ev = out->events[out->n_events];
         ev.iteration = it;
         ev.success = tr.success;
-        ev.batch_size = m;
+        ev.batch_size = M;
         ev.finished_count = tr.finished_count;
         ev.discarded_error = tr.discarded;
         ev.budget_limit = tr.budget_limit;
@@ -579,8 +698,14 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
         t_accepted = tr.threshold;
         fin_e = tr.discarded;  // sum err[final flag == 0]
         fin_v = tr.fin_v;
-        kept = m - tr.finished_count;
-        offsets = ws.off_probe.p;
+        kept = M - tr.finished_count;
+        offsets = sh ? ws.g_off_probe.p : ws.off_probe.p;
+        if (sh) {  // kept offsets of the accepted candidates at rank boundaries
+          PGN_CK(cudaMemcpyAsync(ws.h_kb, ws.g_kb.p, (R + 1) * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, st));
+          PGN_CK(cudaStreamSynchronize(st));
+          for (int r = 0; r <= R; ++r) kb[r] = ws.h_kb[r];
+        }
       }
     }
     row.v = acc_v, row.e = acc_e, row.v_f = acc_vf, row.e_f = acc_ef;
@@ -625,17 +750,62 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       break;
     }
 
-    // ---- fused filter + bisect into the other buffer ---------------------------
+    // ---- fused filter + bisect (+ the exchange that re-balances the shards) ---
     const size_t k4 = kt.mark();
-    launch_split(st, n, m, cap, cap, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p,
-                 ws.err.p, ws.axis.p, ws.low[cur].p, ws.len[cur].p, ws.low[cur ^ 1].p,
-                 ws.len[cur ^ 1].p, ws.pest.p, nullptr);
-    PGN_CK(cudaGetLastError());
+    if (!sh) {
+      launch_split(st, n, m, cap, cap, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p,
+                   ws.err.p, ws.axis.p, ws.low[cur].p, ws.len[cur].p, ws.low[cur ^ 1].p,
+                   ws.len[cur ^ 1].p, ws.pest.p, nullptr);
+      PGN_CK(cudaGetLastError());
+      out->kernel_launches[PAGANI_K_SPLIT]++;
+      m = 2 * kept;
+    } else {
+      const int64_t sc_cap = ws.stage_cap;
+      launch_split(st, n, m, cap, sc_cap, ws.flag.p, use_t ? 1 : 0, t_accepted,
+                   offsets + sh->rb.first[rank], ws.est.p, ws.err.p, ws.axis.p, ws.low[cur].p,
+                   ws.len[cur].p, ws.st_low.p, ws.st_len.p, ws.st_pest.p, nullptr, kb[rank]);
+      PGN_CK(cudaGetLastError());
+      out->kernel_launches[PAGANI_K_SPLIT] += m > 0;
+      const std::vector<int64_t> next = shard_bounds(2 * kept, R);
+      std::vector<Piece> sends, recvs;
+      exchange_plan(R, rank, kb, next, sends, recvs);
+      std::vector<Transfer> ts, tr;
+      double* dlow = ws.low[cur ^ 1].p;
+      double* dlen = ws.len[cur ^ 1].p;
+      for (const Piece& p : sends) {
+        if (p.peer == rank) continue;
+        for (int a = 0; a < n; ++a) {
+          ts.push_back({p.peer, ws.st_low.p + a * sc_cap + p.src_off, p.count * sizeof(double)});
+          ts.push_back({p.peer, ws.st_len.p + a * sc_cap + p.src_off, p.count * sizeof(double)});
+        }
+        ts.push_back({p.peer, ws.st_pest.p + p.src_off, p.count * sizeof(double)});
+      }
+      for (const Piece& p : recvs) {
+        if (p.peer == rank) {  // stays on this GPU: device-to-device copy
+          for (int a = 0; a < n; ++a) {
+            PGN_CK(cudaMemcpyAsync(dlow + a * cap + p.dst_off, ws.st_low.p + a * sc_cap + p.src_off,
+                                   p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            PGN_CK(cudaMemcpyAsync(dlen + a * cap + p.dst_off, ws.st_len.p + a * sc_cap + p.src_off,
+                                   p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+          }
+          PGN_CK(cudaMemcpyAsync(ws.pest.p + p.dst_off, ws.st_pest.p + p.src_off,
+                                 p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+          continue;
+        }
+        for (int a = 0; a < n; ++a) {
+          tr.push_back({p.peer, dlow + a * cap + p.dst_off, p.count * sizeof(double)});
+          tr.push_back({p.peer, dlen + a * cap + p.dst_off, p.count * sizeof(double)});
+        }
+        tr.push_back({p.peer, ws.pest.p + p.dst_off, p.count * sizeof(double)});
+      }
+      comm->exchange(ts, tr, st);
+      sh->set_bounds(next);
+      m = sh->local();
+    }
     kt.span(PAGANI_K_SPLIT, k4, kt.mark());
-    out->kernel_launches[PAGANI_K_SPLIT]++;
     cur ^= 1;
-    m = 2 * kept;
-    out->regions_generated += m;
+    M = 2 * kept;
+    out->regions_generated += M;
     if (m > out->peak_regions) out->peak_regions = m;
   }
   if (!done) finish(PAGANI_MAX_ITERATIONS, cfg.it_max);

@@ -11,8 +11,10 @@
 #include <vector>
 
 #include "../../include/pagani.h"
+#include "comm.hpp"
 #include "kernels.cuh"
 #include "rule.hpp"
+#include "shard.hpp"
 
 namespace pgn {
 
@@ -69,6 +71,17 @@ struct Workspace {
   DevBuf<int64_t> cnt_multi;
   DevBuf<ProbeScalars> d_probe;
   ProbeScalars* h_probe = nullptr;      // pinned
+  // multi-GPU (sharded) buffers: global-order block arrays, records, staging
+  int64_t nb_global_cap = 0, stage_cap = 0;
+  int stage_n = 0;
+  DevBuf<double> g_part, g_err0, g_part_multi, g_scratch_multi, g_scratch;
+  DevBuf<int64_t> g_cnt, g_off, g_off_probe, g_cnt_multi, g_kb;
+  DevBuf<unsigned long long> g_mm;
+  DevBuf<BlockRec> rec_send, rec_recv;
+  DevBuf<ProbeRec> prec_send, prec_recv;
+  DevBuf<double> st_low, st_len, st_pest;
+  int64_t* h_kb = nullptr;  // pinned [kMaxRanks + 1]
+  void ensure_shard(int R, int n, int64_t nb_global, int64_t nblk_max_cap, int64_t stage);
   DevBuf<FoldScalars> d_sc;
   DevBuf<unsigned long long> mm_keys;
   DevBuf<double> mm_out, d_lower, d_step, d_tmp;
@@ -98,6 +111,7 @@ struct ThresholdOutcome {
   double fin_v = 0.0;  // sum of estimates where candidate == 0 (valid on success)
   int minmax_launches = 0;  // kernels launched by min_max (0 or 3)
   int passes = 0;           // speculative probe passes (2 kernels + 1 D2H each)
+  int node = -1;            // accepted node of the last pass
 };
 
 struct Limits {
@@ -105,15 +119,27 @@ struct Limits {
   double p_max_start = 0.25, p_max_step = 0.10, p_max_cap = 0.95;
 };
 
+// Multi-GPU context of one integrate() call (R > 1).
+struct ShardCtx {
+  Comm* comm = nullptr;
+  int R = 1, rank = 0;
+  std::vector<int64_t> bounds;  // global partition of the current batch
+  RankBlocks rb{};
+  int64_t nblk_max = 0, nblk_global = 0;
+  void set_bounds(std::vector<int64_t> b);
+  int64_t first() const { return bounds[rank]; }
+  int64_t local() const { return bounds[rank + 1] - bounds[rank]; }
+};
+
 // classify.cpp:37-95 over device arrays (flags unchanged; candidates are
 // re-derived from the returned threshold).  Leaves, on success, the probe's
-// block offsets in ws.off_probe.
+// block offsets in ws.off_probe (1 GPU) or ws.g_off (sharded, global blocks).
 // minmax: {min, max} of the errors if already known (fused fold), else null.
 ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
                                   const Limits& lim, double* probe_ms,
-                                  const double* minmax = nullptr);
+                                  const double* minmax = nullptr, ShardCtx* sh = nullptr);
 
 void integrate(const pagani_integrand* f, int ndim, const double* lower, const double* upper,
                const pagani_config* cfg, pagani_result* out);

@@ -209,6 +209,79 @@ PGN_HD double gm_cos(double x, const double* __restrict__ SC) {
   return P_DIV(x, x);  // inf or nan -> nan
 }
 
+// Branch-free cos for SIMT: the same glibc arithmetic as gm_cos (every
+// rounded operation identical), but with the paths merged by value selects
+// so the lanes of a warp never diverge between do_sin / do_cos / TAYLOR_SIN /
+// the argument-reduction branches.  Bit-equality with gm_cos (and libm) is
+// checked on 1e8 samples by tests.  Operand-order notes:
+//  * do_cos's s = fma(x*xx, ps, x) and do_sin's s = x + fma(x*xx, ps, dx) share
+//    fma(x*xx, ps, sel) followed by a selected final add;
+//  * do_cos's c = xx*pc equals fma(x, 0, xx*pc) exactly (xx*pc >= +0);
+//  * the three cor fmas differ only in which table entry and sign they take.
+PGN_HD double gm_sel(bool c, double a, double b) { return c ? a : b; }
+
+PGN_HD double gm_cos_bf(double x, const double* __restrict__ SC) {
+  const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
+  const double ax = pgn_fabs(x);
+  // path C: reduce_sincos (|x| < 105414350)
+  const double t = P_FMA(x, PGN_C(kHpinv), PGN_C(kToint));
+  const double xn = P_SUB(t, PGN_C(kToint));
+  const int nq = static_cast<int>(pgn_asu64(t) & 3);
+  const double y = P_FMA(-xn, PGN_C(kMp2), P_FMA(-xn, PGN_C(kMp1), x));
+  const double t2 = P_FMA(-xn, PGN_C(kPp3), y);
+  const double db0 = P_FMA(-xn, PGN_C(kPp3), P_SUB(y, t2));
+  const double bC = P_FMA(-xn, PGN_C(kPp4), t2);
+  const double dbC = P_ADD(db0, P_FMA(-xn, PGN_C(kPp4), P_SUB(t2, bC)));
+  // path B: hp0 - |x|  (0.855469 <= |x| < 2.426265)
+  const double yB = P_SUB(PGN_C(kHp0), ax);
+  const double aB = P_ADD(yB, PGN_C(kHp1));
+  const double daB = P_ADD(P_SUB(yB, aB), PGN_C(kHp1));
+  const bool pA = k < 0x3feb6000u, pB = !pA && k < 0x400368fdu;
+  const double a = pA ? x : (pB ? aB : bC);
+  const double da = pA ? 0.0 : (pB ? daB : dbC);
+  const bool is_cos = pA || (!pB && !(nq & 1));
+  const bool neg = !pA && !pB && ((nq + 1) & 2);
+  // do_sin / do_cos merged
+  const double aa = pgn_fabs(a);
+  const double dx = a < 0 ? -da : da;  // do_sin negates for a <= 0, but a == 0 is TAYLOR there
+  const double u = P_ADD(PGN_C(kBig), aa);
+  const double xr0 = P_SUB(aa, P_SUB(u, PGN_C(kBig)));
+  const double xr = is_cos ? P_ADD(xr0, dx) : xr0;
+  const double xx = P_MUL(xr, xr);
+  const double ps = P_FMA(xx, PGN_C(kSn5), PGN_C(kSn3));
+  const double pc = P_MUL(xx, P_FMA(xx, P_FMA(xx, PGN_C(kCs6), PGN_C(kCs4)), PGN_C(kCs2)));
+  const double sp = P_FMA(P_MUL(xr, xx), ps, is_cos ? xr : dx);
+  const double sv = is_cos ? sp : P_ADD(xr, sp);
+  const double cv = P_FMA(xr, is_cos ? 0.0 : dx, pc);
+  int ki = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  // lanes whose result is discarded below (huge/inf/nan x) may compute any
+  // index: keep the table read in bounds
+  ki = (ki < 0 || ki > 436) ? 0 : ki;
+  const double sn = SC[ki], ssn = SC[ki + 1], cs = SC[ki + 2], ccs = SC[ki + 3];
+  const double A = is_cos ? -sv : sv;
+  double cor = P_FMA(A, is_cos ? ssn : ccs, is_cos ? ccs : ssn);
+  cor = P_FMA(-cv, is_cos ? cs : sn, cor);
+  cor = P_FMA(A, is_cos ? sn : cs, cor);
+  const double r0 = P_ADD(is_cos ? cs : sn, cor);
+  double r = is_cos ? r0
+                    : pgn_asf64((pgn_asu64(r0) & 0x7fffffffffffffffULL) |
+                                (pgn_asu64(a) & 0x8000000000000000ULL));
+  // TAYLOR_SIN branch of do_sin (|a| < 0.126)
+  const double ta = P_MUL(a, a);
+  double p = P_FMA(PGN_C(kS5), ta, PGN_C(kS4));
+  p = P_FMA(p, ta, PGN_C(kS3));
+  p = P_FMA(p, ta, PGN_C(kS2));
+  p = P_FMA(p, ta, PGN_C(kS1));
+  const double tt = P_FMA(ta, P_FMA(p, a, -P_MUL(0.5, da)), da);
+  const double rT = P_ADD(a, tt);
+  r = (!is_cos && aa < PGN_C(kTaylorMax)) ? rT : r;
+  r = neg ? -r : r;
+  // rare: |x| < 2^-27 -> 1; |x| >= 105414350 (not restated) / inf / nan
+  if (k < 0x3e400000u) r = 1.0;
+  if (k >= 0x419921fbu) r = gm_cos(x, SC);
+  return r;
+}
+
 #undef PGN_C
 
 }  // namespace pgn

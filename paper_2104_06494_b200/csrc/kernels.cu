@@ -19,10 +19,10 @@ inline unsigned grid_for(int64_t work, int threads) {
 
 // ---- uniform split ----------------------------------------------------------
 __global__ void k_uniform_split(int n, int d, int64_t m, int64_t cap, double* low, double* len,
-                                const double* lower, const double* step) {
+                                const double* lower, const double* step, int64_t first) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  int64_t rem = j;
+  int64_t rem = first + j;  // global region index
   for (int a = 0; a < n; ++a) {  // geometry.cpp:100-110, axis 0 fastest
     const int64_t cell = rem % d;
     rem /= d;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kSplitThreads)
             int use_t, double t, const int64_t* __restrict__ offsets, const double* __restrict__ est,
             const double* __restrict__ err, const uint8_t* __restrict__ axis,
             const double* __restrict__ low, const double* __restrict__ len, double* dlow,
-            double* dlen, double* dpest, double* dperr) {
+            double* dlen, double* dpest, double* dperr, int64_t kbase) {
   __shared__ int s_warp[kSplitThreads / 32];
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlock;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kSplitThreads)
     const int64_t k = cta_rank(keep, r, carry, s_warp);
     if (!keep) continue;
     const int ax = __ldg(axis + j);
-    const int64_t c0 = 2 * k;
+    const int64_t c0 = 2 * (k - kbase);
     for (int a = 0; a < n; ++a) {  // geometry.cpp:122-141
       const double lo = __ldg(low + a * cap_src + j);
       const double ln = __ldg(len + a * cap_src + j);
@@ -550,7 +550,7 @@ __global__ void k_math(int which, int64_t m, const double* x, double* y) {
   load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  y[j] = which == 0 ? gm_exp(x[j], s_exp) : gm_cos(x[j], s_sc);
+  y[j] = which == 0 ? gm_exp(x[j], s_exp) : (which == 1 ? gm_cos(x[j], s_sc) : gm_cos_bf(x[j], s_sc));
 }
 
 template <class F>
@@ -568,6 +568,122 @@ __global__ void k_call(int n, int64_t m, const double* x, IntegrandParams ip, do
 
 }  // namespace
 
+namespace {
+
+__global__ void k_pack_blocks(int64_t nblk_local, int64_t nblk_max, const double* part,
+                              const int64_t* cnt, const unsigned long long* mm, const double* err,
+                              BlockRec* recs) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    BlockRec h{};
+    h.part[0] = nblk_local > 0 ? err[0] : 0.0;
+    h.cnt = nblk_local;
+    recs[0] = h;
+  }
+  if (i >= nblk_max) return;
+  BlockRec r{};
+  if (i < nblk_local) {
+    for (int q = 0; q < 4; ++q) r.part[q] = part[q * nblk_local + i];
+    r.cnt = cnt[i];
+    r.mn = mm[2 * i];
+    r.mx = mm[2 * i + 1];
+  }
+  recs[1 + i] = r;
+}
+
+__global__ void k_unpack_blocks(RankBlocks rb, int64_t nblk_max, int64_t nblk_global,
+                                const BlockRec* all, double* part, int64_t* cnt,
+                                unsigned long long* mm, double* err0) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) {  // err[0] of the global batch: the first rank owning blocks
+    for (int r = 0; r < rb.R; ++r)
+      if (rb.nblk[r] > 0) {
+        *err0 = all[r * (nblk_max + 1)].part[0];
+        break;
+      }
+  }
+  for (int r = 0; r < rb.R; ++r) {
+    if (i >= rb.nblk[r]) continue;
+    const BlockRec& x = all[r * (nblk_max + 1) + 1 + i];
+    const int64_t g = rb.first[r] + i;
+    for (int q = 0; q < 4; ++q) part[q * nblk_global + g] = x.part[q];
+    cnt[g] = x.cnt;
+    mm[2 * g] = x.mn;
+    mm[2 * g + 1] = x.mx;
+  }
+}
+
+__global__ void k_pack_probe(int64_t nblk_local, int64_t nblk_max, int T, const double* part,
+                             const int64_t* cnt, ProbeRec* recs) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nblk_max) return;
+  ProbeRec r{};
+  if (i < nblk_local)
+    for (int k = 0; k < T; ++k) {
+      r.err_sum[k] = part[(0 * kMaxProbes + k) * nblk_local + i];
+      r.est_sum[k] = part[(1 * kMaxProbes + k) * nblk_local + i];
+      r.cnt[k] = cnt[k * nblk_local + i];
+    }
+  recs[i] = r;
+}
+
+__global__ void k_unpack_probe(RankBlocks rb, int64_t nblk_max, int64_t nblk_global, int T,
+                               const ProbeRec* all, double* part, int64_t* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int r = 0; r < rb.R; ++r) {
+    if (i >= rb.nblk[r]) continue;
+    const ProbeRec& x = all[r * nblk_max + i];
+    const int64_t g = rb.first[r] + i;
+    for (int k = 0; k < T; ++k) {
+      part[(0 * kMaxProbes + k) * nblk_global + g] = x.err_sum[k];
+      part[(1 * kMaxProbes + k) * nblk_global + g] = x.est_sum[k];
+      cnt[k * nblk_global + g] = x.cnt[k];
+    }
+  }
+}
+
+__global__ void k_gather_bounds(RankBlocks rb, const int64_t* offsets, const int64_t* cnt,
+                                int64_t nblk_global, int64_t* out) {
+  const int r = threadIdx.x;
+  if (r < rb.R) out[r] = rb.first[r] < nblk_global ? offsets[rb.first[r]]
+                                                    : (nblk_global ? offsets[nblk_global - 1] +
+                                                                         cnt[nblk_global - 1]
+                                                                   : 0);
+  if (r == rb.R) out[r] = nblk_global ? offsets[nblk_global - 1] + cnt[nblk_global - 1] : 0;
+}
+
+}  // namespace
+
+void launch_pack_blocks(cudaStream_t st, int64_t nblk_local, int64_t nblk_max, const double* part,
+                        const int64_t* cnt, const unsigned long long* mm, const double* err,
+                        BlockRec* recs) {
+  const int64_t w = nblk_max > 0 ? nblk_max : 1;
+  k_pack_blocks<<<grid_for(w, 256), 256, 0, st>>>(nblk_local, nblk_max, part, cnt, mm, err, recs);
+}
+void launch_unpack_blocks(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max,
+                          int64_t nblk_global, const BlockRec* all, double* part, int64_t* cnt,
+                          unsigned long long* mm, double* err0) {
+  const int64_t w = nblk_max > 0 ? nblk_max : 1;
+  k_unpack_blocks<<<grid_for(w, 256), 256, 0, st>>>(rb, nblk_max, nblk_global, all, part, cnt, mm,
+                                                    err0);
+}
+void launch_pack_probe(cudaStream_t st, int64_t nblk_local, int64_t nblk_max, int T,
+                       const double* part, const int64_t* cnt, ProbeRec* recs) {
+  if (nblk_max > 0)
+    k_pack_probe<<<grid_for(nblk_max, 128), 128, 0, st>>>(nblk_local, nblk_max, T, part, cnt, recs);
+}
+void launch_unpack_probe(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max,
+                         int64_t nblk_global, int T, const ProbeRec* all, double* part,
+                         int64_t* cnt) {
+  if (nblk_max > 0)
+    k_unpack_probe<<<grid_for(nblk_max, 128), 128, 0, st>>>(rb, nblk_max, nblk_global, T, all,
+                                                            part, cnt);
+}
+void launch_gather_bounds(cudaStream_t st, const RankBlocks& rb, const int64_t* offsets,
+                          const int64_t* cnt, int64_t nblk_global, int64_t* out) {
+  k_gather_bounds<<<1, kMaxRanks + 1, 0, st>>>(rb, offsets, cnt, nblk_global, out);
+}
+
 const uint64_t* device_exp_table() {
   void* p = nullptr;
   cudaGetSymbolAddress(&p, g_exp_tab);
@@ -580,9 +696,9 @@ const double* device_sincos_table() {
 }
 
 void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap, double* low,
-                          double* len, const double* lower, const double* step) {
+                          double* len, const double* lower, const double* step, int64_t first) {
   if (m <= 0) return;
-  k_uniform_split<<<grid_for(m, 256), 256, 0, st>>>(n, d, m, cap, low, len, lower, step);
+  k_uniform_split<<<grid_for(m, 256), 256, 0, st>>>(n, d, m, cap, low, len, lower, step, first);
 }
 
 void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
@@ -599,6 +715,19 @@ void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const
   if (nblk == 0) return;
   k_probe<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, t, est, err, flag, part,
                                                                  cnt);
+}
+
+void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
+                       const double* err, const uint8_t* flag, double* part, int64_t* cnt) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_probe_multi<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, ts, est, err, flag,
+                                                                       part, cnt);
+}
+
+void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
+                           const int64_t* cnt, double* scratch, ProbeScalars* out) {
+  k_finalize_multi<<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out);
 }
 
 void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
@@ -648,12 +777,12 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
-                  double* dlow, double* dlen, double* dpest, double* dperr) {
+                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   k_split<<<static_cast<unsigned>(nblk), kSplitThreads, 0, st>>>(
       n, m, cap_src, cap_dst, flag, use_t, t, offsets, est, err, axis, low, len, dlow, dlen,
-      dpest, dperr);
+      dpest, dperr, kbase);
 }
 
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,

@@ -48,7 +48,8 @@ struct EvalLaunch {
 // ---- launchers (kernels.cu) ------------------------------------------------
 // uniform_split of the unit cube (geometry.cpp:83-112), axis-major.
 void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap, double* low,
-                          double* len, const double* lower, const double* step);
+                          double* len, const double* lower, const double* step,
+                          int64_t first = 0);
 
 // Post-evaluation block folds: q0 = sum est, q1 = sum err,
 // q2 = sum est[flag==0] (+ count flag==1), q3 = sum err[flag==0].
@@ -86,11 +87,12 @@ void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long lo
 
 // Fused filter (classify.cpp:97-129) + bisect (geometry.cpp:114-143): region
 // j with flag 1 and rank k among the kept writes children 2k, 2k+1 into dst.
+// kbase: subtracted from the (global) kept rank before writing children.
 void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
-                  double* dlow, double* dlen, double* dpest, double* dperr);
+                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase = 0);
 
 // Compaction only (filter() for the batch API).
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
@@ -111,6 +113,45 @@ void launch_serial_volume(cudaStream_t st, int n, int64_t m, int64_t cap, const 
 void launch_math(cudaStream_t st, int which, int64_t m, const double* x, double* y);
 void launch_call_integrand(cudaStream_t st, int fid, int n, int64_t m, const double* x,
                            const IntegrandParams& ip, double* y);
+
+// ---- multi-GPU block records (allgathered once per fold / probe pass) ----
+struct BlockRec {  // per 2048-block fold results of k_evaluate's tail
+  double part[4];
+  long long cnt;
+  unsigned long long mn, mx;
+  double pad;
+};
+struct ProbeRec {  // per 2048-block results of a speculative probe pass
+  double err_sum[kMaxProbes];
+  double est_sum[kMaxProbes];
+  long long cnt[kMaxProbes];
+};
+constexpr int kMaxRanks = 64;
+struct RankBlocks {  // global block index of each rank's first block, and counts
+  int R;
+  int pad;
+  long long first[kMaxRanks];
+  long long nblk[kMaxRanks];
+};
+// recs[0] is a header: part[0] = err[0] of the slice, cnt = #local blocks.
+void launch_pack_blocks(cudaStream_t st, int64_t nblk_local, int64_t nblk_max, const double* part,
+                        const int64_t* cnt, const unsigned long long* mm, const double* err,
+                        BlockRec* recs);
+void launch_unpack_blocks(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max,
+                          int64_t nblk_global, const BlockRec* all, double* part, int64_t* cnt,
+                          unsigned long long* mm, double* err0);
+void launch_pack_probe(cudaStream_t st, int64_t nblk_local, int64_t nblk_max, int T,
+                       const double* part, const int64_t* cnt, ProbeRec* recs);
+void launch_unpack_probe(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max,
+                         int64_t nblk_global, int T, const ProbeRec* all, double* part,
+                         int64_t* cnt);
+void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
+                       const double* err, const uint8_t* flag, double* part, int64_t* cnt);
+void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
+                           const int64_t* cnt, double* scratch, ProbeScalars* out);
+// out[r] = offsets[first_block[r]] (r < R), out[R] = total (from FoldScalars-like count)
+void launch_gather_bounds(cudaStream_t st, const RankBlocks& rb, const int64_t* offsets,
+                          const int64_t* cnt, int64_t nblk_global, int64_t* out);
 
 // Device copies of the glibc tables.
 const uint64_t* device_exp_table();

@@ -72,6 +72,9 @@ def test_device_glibc_exp_cos_bit_exact(pg, gpu, ref):
         libm(C.c_int64(len(xs)), xs.ctypes.data_as(C.POINTER(C.c_double)),
              want.ctypes.data_as(C.POINTER(C.c_double)))
         assert np.array_equal(bits(got), bits(want))
+        if fn is pg.glibc_cos:
+            assert np.array_equal(bits(pg.glibc_cos(xs, on_device=True, branch_free=True)),
+                                  bits(want))
 
 
 # ------------------------------------------------------ evaluate ----------

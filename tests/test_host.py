@@ -91,6 +91,13 @@ def test_host_glibc_restatement_matches_libm(pg, ref):
     ref.lib.ref_libm_cos(C.c_int64(len(cs)), cs.ctypes.data_as(C.POINTER(C.c_double)),
                          libm.ctypes.data_as(C.POINTER(C.c_double)))
     assert np.array_equal(bits(mine), bits(libm))
+    # the branch-free SIMT variant (f1's fin) is the same function
+    assert np.array_equal(bits(pg.glibc_cos(cs, on_device=False, branch_free=True)), bits(libm))
+    sweep = np.arange(-20.0, 20.0, 2.5e-6)  # every quadrant / table boundary, densely
+    want = np.empty_like(sweep)
+    ref.lib.ref_libm_cos(C.c_int64(len(sweep)), sweep.ctypes.data_as(C.POINTER(C.c_double)),
+                         want.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(bits(pg.glibc_cos(sweep, on_device=False, branch_free=True)), bits(want))
 
 
 def test_scalar_helpers_match_reference(pg, ref):
