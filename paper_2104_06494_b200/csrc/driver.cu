@@ -16,6 +16,7 @@
 #include "driver.hpp"
 
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -429,8 +430,9 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   const DeviceIntegrand di = resolve_integrand(f);
   if (cfg.mode != PAGANI_MODE_PARITY && cfg.mode != PAGANI_MODE_FAST)
     throw std::invalid_argument("Config: unknown mode");
-  const EvalLaunch eval_k = lookup_evaluate(di.fid, n, cfg.mode);
+  EvalLaunch eval_k = lookup_evaluate(di.fid, n, cfg.mode);
   if (!eval_k.fn) throw UnsupportedError("no device kernel for this integrand/dimension");
+  if (std::getenv("PAGANI_UNFUSED_FOLD")) eval_k.fused_fold = false;  // A/B experiments
 
   // ---- ranks ------------------------------------------------------------------
   Comm* comm = comm_from_handle(cfg.comm);

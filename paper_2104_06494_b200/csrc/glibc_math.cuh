@@ -36,6 +36,48 @@ constexpr uint64_t kC4 = 0x3fa55555cf172b91ULL;
 constexpr uint64_t kC5 = 0x3f81111167a4d017ULL;
 }  // namespace expc
 
+// cos constants (s_sin.c / usncs.h)
+namespace cosc {
+constexpr uint64_t kBig = 0x42c8000000000000ULL;    // 0x1.8p45
+constexpr uint64_t kSn3 = 0xbfc5555555555515ULL;
+constexpr uint64_t kSn5 = 0x3f811110e829872fULL;
+constexpr uint64_t kCs2 = 0x3fe0000000000000ULL;
+constexpr uint64_t kCs4 = 0xbfa5555555555535ULL;
+constexpr uint64_t kCs6 = 0x3f56c16bedd9e239ULL;
+constexpr uint64_t kS1 = 0xbfc5555555555555ULL;
+constexpr uint64_t kS2 = 0x3f81111111110eceULL;
+constexpr uint64_t kS3 = 0xbf2a01a019db08b8ULL;
+constexpr uint64_t kS4 = 0x3ec71de27b9a7ed9ULL;
+constexpr uint64_t kS5 = 0xbe5addffc2fcdf59ULL;
+constexpr uint64_t kHp0 = 0x3ff921fb54442d18ULL;
+constexpr uint64_t kHp1 = 0x3c91a62633145c07ULL;
+constexpr uint64_t kToint = 0x4338000000000000ULL;
+constexpr uint64_t kHpinv = 0x3fe45f306dc9c883ULL;
+constexpr uint64_t kMp1 = 0x3ff921fb58000000ULL;
+constexpr uint64_t kMp2 = 0xbe4dde973c000000ULL;
+constexpr uint64_t kPp3 = 0xbc8cb3b398000000ULL;
+constexpr uint64_t kPp4 = 0xbacd747f23e32ed7ULL;
+constexpr uint64_t kTaylorMax = 0x3fc020c49ba5e354ULL;  // 0.126
+}  // namespace cosc
+
+// Optionally (PGN_GM_CONSTANT_BANK) the device reads the constants from a
+// __constant__ table as constant-bank operands instead of 64-bit immediates;
+// measured neutral-to-slower on B200 (f6 8D k_evaluate +3%), so immediates are
+// the default.  Same bit patterns either way.
+enum GmConst {
+  kGm_expc_kInvLn2N, kGm_expc_kShift, kGm_expc_kNegLn2hiN, kGm_expc_kNegLn2loN, kGm_expc_kC2, kGm_expc_kC3, kGm_expc_kC4, kGm_expc_kC5, kGm_cosc_kBig, kGm_cosc_kSn3, kGm_cosc_kSn5, kGm_cosc_kCs2, kGm_cosc_kCs4, kGm_cosc_kCs6, kGm_cosc_kS1, kGm_cosc_kS2, kGm_cosc_kS3, kGm_cosc_kS4, kGm_cosc_kS5, kGm_cosc_kHp0, kGm_cosc_kHp1, kGm_cosc_kToint, kGm_cosc_kHpinv, kGm_cosc_kMp1, kGm_cosc_kMp2, kGm_cosc_kPp3, kGm_cosc_kPp4, kGm_cosc_kTaylorMax, kGmCount
+};
+#if defined(__CUDACC__)
+static __constant__ uint64_t c_gm[kGmCount] = {
+    expc::kInvLn2N, expc::kShift, expc::kNegLn2hiN, expc::kNegLn2loN, expc::kC2, expc::kC3, expc::kC4, expc::kC5, cosc::kBig, cosc::kSn3, cosc::kSn5, cosc::kCs2, cosc::kCs4, cosc::kCs6, cosc::kS1, cosc::kS2, cosc::kS3, cosc::kS4, cosc::kS5, cosc::kHp0, cosc::kHp1, cosc::kToint, cosc::kHpinv, cosc::kMp1, cosc::kMp2, cosc::kPp3, cosc::kPp4, cosc::kTaylorMax};
+#endif
+#if defined(__CUDA_ARCH__) && defined(PGN_GM_CONSTANT_BANK)
+#define PGN_GM(ns, name) __longlong_as_double(static_cast<long long>(c_gm[kGm_##ns##_##name]))
+#else
+#define PGN_GM(ns, name) pgn_asf64(ns::name)
+#endif
+#define PGN_C(name) PGN_GM(cosc, name)
+
 // e_exp.c specialcase(): result near the overflow/underflow boundaries.
 PGN_HD double gm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
   if ((ki & 0x80000000ULL) == 0) {
@@ -74,19 +116,19 @@ PGN_HD double gm_exp(double x, const uint64_t* __restrict__ T) {
     }
     abstop = 0;  // large |x|: handled by the special case below
   }
-  double kd = P_FMA(x, pgn_asf64(kInvLn2N), pgn_asf64(kShift));
+  double kd = P_FMA(x, PGN_GM(expc, kInvLn2N), PGN_GM(expc, kShift));
   const uint64_t ki = pgn_asu64(kd);
-  kd = P_SUB(kd, pgn_asf64(kShift));
-  double r = P_FMA(kd, pgn_asf64(kNegLn2hiN), x);
-  r = P_FMA(kd, pgn_asf64(kNegLn2loN), r);
+  kd = P_SUB(kd, PGN_GM(expc, kShift));
+  double r = P_FMA(kd, PGN_GM(expc, kNegLn2hiN), x);
+  r = P_FMA(kd, PGN_GM(expc, kNegLn2loN), r);
   const uint64_t idx = 2 * (ki & 127);
   const uint64_t top = ki << 45;
   const double tail = pgn_asf64(T[idx]);
   const uint64_t sbits = T[idx + 1] + top;
-  const double p23 = P_FMA(r, pgn_asf64(kC3), pgn_asf64(kC2));
+  const double p23 = P_FMA(r, PGN_GM(expc, kC3), PGN_GM(expc, kC2));
   const double tr = P_ADD(r, tail);
   const double r2 = P_MUL(r, r);
-  const double p45 = P_FMA(r, pgn_asf64(kC5), pgn_asf64(kC4));
+  const double p45 = P_FMA(r, PGN_GM(expc, kC5), PGN_GM(expc, kC4));
   const double t = P_FMA(p23, r2, tr);
   const double r4 = P_MUL(r2, r2);
   const double tmp = P_FMA(r4, p45, t);
@@ -96,30 +138,6 @@ PGN_HD double gm_exp(double x, const uint64_t* __restrict__ T) {
 }
 
 // ---- cos: sysdeps/ieee754/dbl-64/s_sin.c (glibc 2.39), __cos_fma ---------
-namespace cosc {
-constexpr uint64_t kBig = 0x42c8000000000000ULL;    // 0x1.8p45
-constexpr uint64_t kSn3 = 0xbfc5555555555515ULL;
-constexpr uint64_t kSn5 = 0x3f811110e829872fULL;
-constexpr uint64_t kCs2 = 0x3fe0000000000000ULL;
-constexpr uint64_t kCs4 = 0xbfa5555555555535ULL;
-constexpr uint64_t kCs6 = 0x3f56c16bedd9e239ULL;
-constexpr uint64_t kS1 = 0xbfc5555555555555ULL;
-constexpr uint64_t kS2 = 0x3f81111111110eceULL;
-constexpr uint64_t kS3 = 0xbf2a01a019db08b8ULL;
-constexpr uint64_t kS4 = 0x3ec71de27b9a7ed9ULL;
-constexpr uint64_t kS5 = 0xbe5addffc2fcdf59ULL;
-constexpr uint64_t kHp0 = 0x3ff921fb54442d18ULL;
-constexpr uint64_t kHp1 = 0x3c91a62633145c07ULL;
-constexpr uint64_t kToint = 0x4338000000000000ULL;
-constexpr uint64_t kHpinv = 0x3fe45f306dc9c883ULL;
-constexpr uint64_t kMp1 = 0x3ff921fb58000000ULL;
-constexpr uint64_t kMp2 = 0xbe4dde973c000000ULL;
-constexpr uint64_t kPp3 = 0xbc8cb3b398000000ULL;
-constexpr uint64_t kPp4 = 0xbacd747f23e32ed7ULL;
-constexpr uint64_t kTaylorMax = 0x3fc020c49ba5e354ULL;  // 0.126
-}  // namespace cosc
-
-#define PGN_C(name) pgn_asf64(cosc::name)
 
 // s_sin.c do_cos(x, dx)
 PGN_HD double gm_do_cos(double x, double dx, const double* __restrict__ SC) {
