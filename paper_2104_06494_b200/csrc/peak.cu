@@ -8,22 +8,34 @@ namespace {
 
 constexpr int kChains = 8;
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(256) k_dfma_peak(double* out, long long* cycles, int iters,
                                                    double a, double b) {
   double x[kChains];
 #pragma unroll
   for (int c = 0; c < kChains; ++c) x[c] = 1.0 + 1e-3 * (threadIdx.x + c);
+  const unsigned long long g0 = globaltimer_ns();
   const long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int c = 0; c < kChains; ++c) x[c] = __fma_rn(x[c], a, b);
   }
   const long long t1 = clock64();
+  const unsigned long long g1 = globaltimer_ns();
   double s = 0.0;
 #pragma unroll
   for (int c = 0; c < kChains; ++c) s += x[c];
   if (s == 12345.678) out[0] = s;  // keep the chains alive
-  if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+  // SM clock of this CTA's own span (cycles / ns); the kernel may run in waves
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    cycles[0] = t1 - t0;
+    cycles[1] = static_cast<long long>(g1 - g0);
+  }
 }
 
 }  // namespace
@@ -35,7 +47,7 @@ extern "C" int pagani_fp64_peak(int device, double seconds, double* tflops, doub
     PGN_CK(cudaGetDeviceProperties(&prop, device));
     const int blocks = prop.multiProcessorCount * 8;
     pgn::DevBuf<double> out(1);
-    pgn::DevBuf<long long> cyc(1);
+    pgn::DevBuf<long long> cyc(2);
     cudaEvent_t e0, e1;
     PGN_CK(cudaEventCreate(&e0));
     PGN_CK(cudaEventCreate(&e1));
@@ -52,11 +64,13 @@ extern "C" int pagani_fp64_peak(int device, double seconds, double* tflops, doub
       const double scale = (1e3 * seconds) / (ms > 0.01f ? ms : 0.01f);
       iters = static_cast<int>(iters * (scale > 64 ? 64 : (scale < 1.1 ? 1.1 : scale)));
     }
-    long long cycles = 0;
-    PGN_CK(cudaMemcpy(&cycles, cyc.p, sizeof cycles, cudaMemcpyDeviceToHost));
+    long long cyc_ns[2] = {0, 1};
+    PGN_CK(cudaMemcpy(cyc_ns, cyc.p, sizeof cyc_ns, cudaMemcpyDeviceToHost));
     const double flops = 2.0 * kChains * static_cast<double>(iters) * blocks * 256.0;
     *tflops = flops / (ms * 1e-3) / 1e12;
-    if (sm_mhz) *sm_mhz = static_cast<double>(cycles) / (ms * 1e-3) / 1e6;
+    if (sm_mhz)
+      *sm_mhz = cyc_ns[1] > 0 ? 1e3 * static_cast<double>(cyc_ns[0]) / static_cast<double>(cyc_ns[1])
+                              : 0.0;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return PAGANI_OK;

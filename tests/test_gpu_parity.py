@@ -94,6 +94,29 @@ def test_evaluate_batch_bit_exact(pg, gpu, ref, fid):
         assert cnt == c2
 
 
+def test_evaluate_batch_nonfinite_and_overflow(pg, gpu, ref):
+    """The separable evaluator tracks rule.cpp:384's `finite` flag lazily (a
+    non-finite S[0] triggers an exact re-walk of the region's points): regions
+    with inf/NaN point values AND regions whose finite values overflow the
+    weighted sums (finite=true, est=+-inf) must both match the reference."""
+    rng = np.random.default_rng(77)
+    for fid, n, scale in ((7, 3, 1e14), (7, 5, 3e13), (8, 4, 1e21), (3, 2, 1.0), (3, 3, 1.0)):
+        m = 600
+        if fid == 3:  # 1 + x0 + 2 x1 (+ 3 x2) crosses 0: huge / inf / NaN values
+            lows = rng.uniform(-2.0, 0.5, size=(m, n))
+            lens = rng.uniform(0.01, 1.5, size=(m, n))
+        else:  # point values from ~1e250 to inf: overflowing sums and inf points
+            lows = rng.uniform(0.0, scale, size=(m, n))
+            lens = rng.uniform(0.01, 1.0, size=(m, n)) * scale
+        est, raw, axes, cnt = pg.evaluate_batch(pg.Integrand(fid), lows, lens)
+        e2, r2, a2, c2 = ref.evaluate_batch(fid, lows, lens)
+        assert np.array_equal(bits(est), bits(e2)), (fid, n)
+        assert np.array_equal(bits(raw), bits(r2)), (fid, n)
+        assert np.array_equal(axes, a2), (fid, n)
+        if fid != 3:  # inf points and overflowing finite sums both occur
+            assert (~np.isfinite(r2)).any() and (np.isinf(e2)).any(), (fid, n)
+
+
 def test_evaluate_batch_n16_and_unit_cube_splits(pg, gpu, ref):
     for fid in (3, 4, 5):
         lows, lens = ref.uniform_split([0.0] * 16, [1.0] * 16, 1)
