@@ -281,6 +281,7 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
       ps.t[2 * k + 1] = (ps.t[k] + max_err) * 0.5;
       ps.t[2 * k + 2] = (ps.t[k] + min_err) * 0.5;
     }
+    prepare_probes(ps);
     cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
     if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
     if (!sh) {

@@ -102,7 +102,24 @@ PGN_HD double gm_exp_special(double tmp, uint64_t sbits, uint64_t ki) {
   return P_MUL(0x1p-1022, y);
 }
 
+// exp's polynomial / reduction constants as values.  By default they are the
+// immediates below (so nvcc folds them); the evaluator can instead load them
+// once per thread into registers (PGN_HOIST_EXP) so the hot loops do not
+// re-materialise 64-bit immediates (2 MOVs each) on every call.
+struct ExpK {
+  double inv_ln2_n = pgn_asf64(expc::kInvLn2N);
+  double neg_ln2hi_n = pgn_asf64(expc::kNegLn2hiN);
+  double neg_ln2lo_n = pgn_asf64(expc::kNegLn2loN);
+  double c2 = pgn_asf64(expc::kC2);
+  double c3 = pgn_asf64(expc::kC3);
+  double c4 = pgn_asf64(expc::kC4);
+  double c5 = pgn_asf64(expc::kC5);
+};
+
+PGN_HD double gm_exp_k(double x, const uint64_t* __restrict__ T, const ExpK& K);
+
 PGN_HD double gm_exp(double x, const uint64_t* __restrict__ T) {
+#if defined(PGN_GM_CONSTANT_BANK) && defined(__CUDA_ARCH__)
   using namespace expc;
   const uint64_t ix = pgn_asu64(x);
   uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ff;
@@ -129,6 +146,44 @@ PGN_HD double gm_exp(double x, const uint64_t* __restrict__ T) {
   const double tr = P_ADD(r, tail);
   const double r2 = P_MUL(r, r);
   const double p45 = P_FMA(r, PGN_GM(expc, kC5), PGN_GM(expc, kC4));
+  const double t = P_FMA(p23, r2, tr);
+  const double r4 = P_MUL(r2, r2);
+  const double tmp = P_FMA(r4, p45, t);
+  if (abstop == 0) return gm_exp_special(tmp, sbits, ki);
+  const double scale = pgn_asf64(sbits);
+  return P_FMA(scale, tmp, scale);
+#else
+  return gm_exp_k(x, T, ExpK{});
+#endif
+}
+
+PGN_HD double gm_exp_k(double x, const uint64_t* __restrict__ T, const ExpK& K) {
+  using namespace expc;
+  const uint64_t ix = pgn_asu64(x);
+  uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ff;
+  if (abstop - 0x3c9u >= 0x3fu) {
+    if (static_cast<int32_t>(abstop - 0x3c9u) < 0) return P_ADD(1.0, x);  // |x| < 2^-54
+    if (abstop >= 0x409u) {                                               // |x| >= 1024
+      if (ix == 0xfff0000000000000ULL) return 0.0;
+      if (abstop >= 0x7ffu) return P_ADD(1.0, x);
+      if (ix >> 63) return 0.0;                          // __math_uflow(0)
+      return pgn_asf64(0x7ff0000000000000ULL);           // __math_oflow(0)
+    }
+    abstop = 0;  // large |x|: handled by the special case below
+  }
+  double kd = P_FMA(x, K.inv_ln2_n, PGN_GM(expc, kShift));
+  const uint64_t ki = pgn_asu64(kd);
+  kd = P_SUB(kd, PGN_GM(expc, kShift));
+  double r = P_FMA(kd, K.neg_ln2hi_n, x);
+  r = P_FMA(kd, K.neg_ln2lo_n, r);
+  const uint64_t idx = 2 * (ki & 127);
+  const uint64_t top = ki << 45;
+  const double tail = pgn_asf64(T[idx]);
+  const uint64_t sbits = T[idx + 1] + top;
+  const double p23 = P_FMA(r, K.c3, K.c2);
+  const double tr = P_ADD(r, tail);
+  const double r2 = P_MUL(r, r);
+  const double p45 = P_FMA(r, K.c5, K.c4);
   const double t = P_FMA(p23, r2, tr);
   const double r4 = P_MUL(r2, r2);
   const double tmp = P_FMA(r4, p45, t);

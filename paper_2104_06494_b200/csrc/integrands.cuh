@@ -19,11 +19,16 @@
 #include "fp_ops.cuh"
 #include "glibc_math.cuh"
 
+#ifndef PGN_F1_COS_BF
+#define PGN_F1_COS_BF 0
+#endif
+
 namespace pgn {
 
 struct MathTables {
   const uint64_t* exp_tab;  // 256 u64 (glibc __exp_data.tab)
   const double* sincos;     // 440 doubles (glibc __sincostab)
+  ExpK K{};                 // exp constants (immediates unless the kernel hoists them)
 };
 
 struct IntegrandParams {
@@ -49,7 +54,13 @@ struct F1 {  // cos(sum (i+1) x_i)              integrands.cpp:24-28
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 1), x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
-  PGN_HD static double fin(double s, int, const MathTables& T) { return gm_cos(s, T.sincos); }
+  PGN_HD static double fin(double s, int, const MathTables& T) {
+#if PGN_F1_COS_BF
+    return gm_cos_bf(s, T.sincos);
+#else
+    return gm_cos(s, T.sincos);
+#endif
+  }
   PGN_HD static bool cut(int, double) { return false; }
 };
 
@@ -85,7 +96,7 @@ struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
-    return gm_exp(P_MUL(-625.0, s), T.exp_tab);
+    return gm_exp_k(P_MUL(-625.0, s), T.exp_tab, T.K);
   }
   PGN_HD static bool cut(int, double) { return false; }
 };
@@ -96,7 +107,7 @@ struct F5 {  // exp(-10 sum |x-1/2|)             integrands.cpp:54-58
   PGN_HD static double term(int, double x) { return pgn_fabs(P_SUB(x, 0.5)); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
-    return gm_exp(P_MUL(-10.0, s), T.exp_tab);
+    return gm_exp_k(P_MUL(-10.0, s), T.exp_tab, T.K);
   }
   PGN_HD static bool cut(int, double) { return false; }
 };
@@ -106,7 +117,9 @@ struct F6 {  // exp(sum (i+5) x_i), 0 outside    integrands.cpp:60-67
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 5), x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
-  PGN_HD static double fin(double s, int, const MathTables& T) { return gm_exp(s, T.exp_tab); }
+  PGN_HD static double fin(double s, int, const MathTables& T) {
+    return gm_exp_k(s, T.exp_tab, T.K);
+  }
   PGN_HD static bool cut(int a, double x) {
     return x >= P_DIV(P_ADD(3.0, static_cast<double>(a + 1)), 10.0);
   }

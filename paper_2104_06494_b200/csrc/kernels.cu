@@ -4,6 +4,9 @@
 // as 16-byte pairs (2k, 2k+1).
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <limits>
+
 #include "glibc_tables.h"
 
 namespace pgn {
@@ -161,38 +164,179 @@ __global__ void __launch_bounds__(kFoldThreads)
   part[(threadIdx.x == 0 ? 0 : 1) * nblk + b] = fin;
 }
 
+// Pairwise tree (reduce.cpp:13-27: p[i] = p[2i] + p[2i+1], odd tail carried)
+// of src[0..n) by a group of gn threads (local id lt).  The first level reads
+// the global partials, every later level runs in shared memory (`sm`, room for
+// n + 64 doubles): one __syncthreads per level instead of an L2 round trip.
+// Every thread of the CTA must call it with the same n (it syncs the CTA).
+__device__ __forceinline__ double tree_sum_smem(const double* src, int64_t n, double* sm, int lt,
+                                                int gn) {
+  if (n <= 0) return 0.0;
+  const double* s = src;
+  double* d = sm;
+  int64_t cur = n;
+  while (cur > 1) {
+    const int64_t half = cur / 2;
+    for (int64_t i = lt; i < half; i += gn) d[i] = P_ADD(s[2 * i], s[2 * i + 1]);
+    if ((cur & 1) && lt == 0) d[half] = s[cur - 1];
+    __syncthreads();
+    cur = half + (cur & 1);
+    s = d;
+    d += cur;
+  }
+  return s[0];
+}
+// Shared-memory trees are used while they fit: doubles per tree = nblk + 64.
+constexpr int64_t kTreeSmemMaxBytes = 200 * 1024;
+inline size_t tree_smem_bytes(int64_t nblk, int groups) {
+  return static_cast<size_t>(groups) * static_cast<size_t>(nblk + 64) * sizeof(double);
+}
+
 // Speculative threshold probes: T <= kMaxProbes candidate thresholds (a
 // level-order tree of the search's possible next steps, classify.cpp:82-89)
-// evaluated in ONE pass.  The block is staged in smem once; lane i of warp 0
-// folds err where cand_i == 0 and counts cand_i == 1, lane i of warp 1 folds
-// est where cand_i == 0 -- T serial chains in the latency of one.
-__global__ void __launch_bounds__(kFoldThreads)
-    k_probe_multi(int64_t m, int64_t nblk, ProbeSet ts, const double* __restrict__ est,
+// evaluated in ONE pass over the block.
+//
+// Per 2048-block the result is 2T strict serial folds (sum err / sum est over
+// the non-candidates of each threshold, reduce.cpp:54-62) -- dependent DADD
+// chains, so the kernel is built around keeping 30 chains busy on ONE warp:
+// lane j < 15 folds err for node j, lane 16+j folds est for node j.  The
+// candidate test is one predicate-producing LOP3: producers give every region
+// a code (flag ? #{sorted thresholds the error reaches} : 0, see ProbeSet),
+// stored as the 16-bit mask (1 << code) - 1 over sorted positions, and node
+// j's candidates are exactly the regions with bit pos[j] set.  Each step is
+// then LOP3 + 2 FSEL + DADD + IADD (+ 3/8 LDS.128); the err lanes' counters
+// are the candidate counts.
+//
+// Streaming: warps 1..3 stage chunk c+1 (est, err, code; 17 B/region) into a
+// 2-deep shared-memory ring while warp 0 folds chunk c, so a CTA needs only
+// 13.9 KB and every block of a 2^22-region batch is resident at once.
+constexpr int kProbeThreads = 128;
+constexpr int kProbeChunk = 384;  // = 4 x 96 producer threads = 3 x 128
+struct ProbeStage {
+  double err[2][kProbeChunk];
+  double est[2][kProbeChunk];
+  uint16_t mask[2][kProbeChunk];
+  double s[16];
+};
+
+// ss: the 16 sorted thresholds in shared memory (lane-divergent indices would
+// serialise in the constant cache).
+__device__ __forceinline__ uint8_t probe_code(const double* ss, int nan_cnt, uint8_t f, double e) {
+  if (!f) return 0;
+  if (e != e) return 16;
+  int p = 0;  // upper bound over 16 sorted entries (NaN padding compares false)
+#pragma unroll
+  for (int step = 8; step > 0; step >>= 1)
+    if (ss[p + step - 1] <= e) p += step;
+  return static_cast<uint8_t>(nan_cnt + p);
+}
+
+// Stage chunk c (kProbeChunk regions) into ring slot c & 1: nt threads, PER
+// regions each (nt * PER == kProbeChunk); all loads are issued before any use.
+template <int PER>
+__device__ __forceinline__ void probe_stage_chunk(ProbeStage& S, const ProbeSet& ts,
+                                                  const double* __restrict__ est,
+                                                  const double* __restrict__ err,
+                                                  const uint8_t* __restrict__ flag, int64_t lo,
+                                                  int n, int c, int t0, int nt) {
+  const int buf = c & 1;
+  double e[PER], v[PER];
+  uint8_t f[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = c * kProbeChunk + t0 + u * nt;
+    e[u] = 0.0;
+    v[u] = 0.0;
+    f[u] = 0;
+    if (k < n) {
+      e[u] = __ldg(err + lo + k);
+      v[u] = __ldg(est + lo + k);
+      f[u] = __ldg(flag + lo + k);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = t0 + u * nt;
+    const uint8_t code = probe_code(S.s, ts.nan_cnt, f[u], e[u]);
+    S.err[buf][i] = e[u];
+    S.est[buf][i] = v[u];
+    S.mask[buf][i] = static_cast<uint16_t>((1u << code) - 1u);
+  }
+}
+
+// s += v unless (word & bit) (the skip of reduce.cpp:59-60; adding +0.0
+// instead is identical: s starts at +0.0 and never becomes -0.0 under RN).
+// The select happens on the loaded value, off the DADD dependency chain.
+__device__ __forceinline__ void add_unless(double& s, double v, uint32_t word, uint32_t bit,
+                                           int& c) {
+  const bool cand = (word & bit) != 0;
+  c += cand;
+  s = P_ADD(s, cand ? 0.0 : v);
+}
+
+__global__ void __launch_bounds__(kProbeThreads)
+    k_probe_multi(int64_t m, int64_t nblk, const ProbeSet ts, const double* __restrict__ est,
                   const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
                   int64_t* cnt) {
-  __shared__ FoldSmem S;
+  __shared__ __align__(16) ProbeStage S;
   const int64_t b = blockIdx.x;
   const int64_t lo = b * kBlock;
   const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
-  stage_block(S, est, err, flag, lo, n, true, 0.0, false);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (w > 1 || lane >= ts.T) return;
-  const double t = ts.t[lane];
-  const double* x = w == 0 ? S.err : S.est;
+  const int nch = (n + kProbeChunk - 1) / kProbeChunk;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < 16) S.s[tid] = ts.s[tid];
+  __syncthreads();
+  probe_stage_chunk<kProbeChunk / kProbeThreads>(S, ts, est, err, flag, lo, n, 0, tid,
+                                                 kProbeThreads);
+  __syncthreads();
+  const int node = (lane & 15) < ts.T ? (lane & 15) : 0;
+  const int pos = ts.pos[node];
+  const int q = lane >> 4;  // 0: err chain, 1: est chain
   double fin = 0.0;
-  int64_t c = 0;
-#pragma unroll 8
-  for (int i = 0; i < n; ++i) {
-    const bool c1 = S.flag[i] && !(S.err[i] < t);
-    c += c1;
-    fin = P_ADD(fin, c1 ? 0.0 : x[i]);
+  int cc = 0;  // candidates of node `node` in this block
+  for (int c = 0; c < nch; ++c) {
+    if (w > 0) {
+      if (c + 1 < nch)
+        probe_stage_chunk<kProbeChunk / (kProbeThreads - 32)>(S, ts, est, err, flag, lo, n, c + 1,
+                                                              tid - 32, kProbeThreads - 32);
+    } else {
+      const int buf = c & 1;
+      const double* x = q ? S.est[buf] : S.err[buf];
+      const uint16_t* mk = S.mask[buf];
+      const int cntc = n - c * kProbeChunk < kProbeChunk ? n - c * kProbeChunk : kProbeChunk;
+      if (cntc == kProbeChunk) {
+        const uint32_t blo = 1u << pos, bhi = blo << 16;
+#pragma unroll 2
+        for (int i = 0; i < kProbeChunk; i += 8) {
+          const uint4 m8 = *reinterpret_cast<const uint4*>(mk + i);
+          const double2 v0 = *reinterpret_cast<const double2*>(x + i);
+          const double2 v1 = *reinterpret_cast<const double2*>(x + i + 2);
+          const double2 v2 = *reinterpret_cast<const double2*>(x + i + 4);
+          const double2 v3 = *reinterpret_cast<const double2*>(x + i + 6);
+          add_unless(fin, v0.x, m8.x, blo, cc);
+          add_unless(fin, v0.y, m8.x, bhi, cc);
+          add_unless(fin, v1.x, m8.y, blo, cc);
+          add_unless(fin, v1.y, m8.y, bhi, cc);
+          add_unless(fin, v2.x, m8.z, blo, cc);
+          add_unless(fin, v2.y, m8.z, bhi, cc);
+          add_unless(fin, v3.x, m8.w, blo, cc);
+          add_unless(fin, v3.y, m8.w, bhi, cc);
+        }
+      } else {
+        for (int i = 0; i < cntc; ++i) add_unless(fin, x[i], mk[i], 1u << pos, cc);
+      }
+    }
+    __syncthreads();
   }
-  part[(w * kMaxProbes + lane) * nblk + b] = fin;
-  if (w == 0) cnt[lane * nblk + b] = c;
+  if (w == 0 && (lane & 15) < ts.T) {
+    part[(q * kMaxProbes + node) * nblk + b] = fin;
+    if (q == 0) cnt[node * nblk + b] = cc;
+  }
 }
 
 // Pairwise trees (reduce.cpp:13-27) for 2T fold arrays + T count totals:
 // one CTA per array.
+template <bool SMEM>
 __global__ void __launch_bounds__(256)
     k_finalize_multi(int64_t nblk, int T, const double* part, const int64_t* cnt, double* scratch,
                      ProbeScalars* out) {
@@ -214,6 +358,12 @@ __global__ void __launch_bounds__(256)
   }
   const int w = id / T, i = id % T;
   const double* src = part + (w * kMaxProbes + i) * nblk;
+  if (SMEM) {
+    extern __shared__ double s_tree[];
+    const double v = tree_sum_smem(src, nblk, s_tree, tid, 256);
+    if (tid == 0) (w == 0 ? out->err_sum : out->est_sum)[i] = v;
+    return;
+  }
   double* bufs[2] = {scratch + static_cast<int64_t>(id) * 2 * nblk,
                      scratch + static_cast<int64_t>(id) * 2 * nblk + nblk};
   int cur_buf = 0;
@@ -277,10 +427,13 @@ __global__ void k_fold_one(int64_t m, int64_t nblk, const double* __restrict__ x
 // ---- pairwise tree + offsets (single CTA) -----------------------------------
 constexpr int kFinThreads = 1024;
 
+
+template <bool SMEM>
 __global__ void __launch_bounds__(kFinThreads)
     k_finalize(int64_t nblk, int nq, const double* part, const int64_t* cnt, int64_t* offsets,
                double* scratch, FoldScalars* out, const unsigned long long* mm,
                const double* err0) {
+  extern __shared__ double s_tree[];
   __shared__ int64_t s_sum[kFinThreads];
   __shared__ unsigned long long s_k[2][kFinThreads / 32];
   const int tid = threadIdx.x;
@@ -317,6 +470,14 @@ __global__ void __launch_bounds__(kFinThreads)
     }
   }
   // reduce.cpp:13-27: p[i] = p[2i] + p[2i+1] level by level, odd tail carried.
+  if constexpr (SMEM) {  // the nq <= 4 trees side by side, one 256-thread group each
+    constexpr int G = kFinThreads / 4;
+    const int q = tid / G;
+    const double v = tree_sum_smem(part + (q < nq ? q : 0) * nblk, nblk,
+                                   s_tree + q * (nblk + 64), tid % G, G);
+    if (q < nq && tid % G == 0) out->sum[q] = v;
+    __syncthreads();
+  } else
   for (int q = 0; q < nq; ++q) {
     const double* src = part + q * nblk;
     double* bufs[2] = {scratch, scratch + nblk};
@@ -717,17 +878,44 @@ void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const
                                                                  cnt);
 }
 
+void finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
+                    const int64_t* cnt, double* scratch, ProbeScalars* out) {
+  const size_t sm = tree_smem_bytes(nblk, 1);
+  if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
+    // opt in to > 48 KB dynamic shared memory (per device; cheap host call)
+    cudaFuncSetAttribute(k_finalize_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kTreeSmemMaxBytes));
+    k_finalize_multi<true><<<3 * T, 256, sm, st>>>(nblk, T, part, cnt, scratch, out);
+  } else {
+    k_finalize_multi<false><<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out);
+  }
+}
+
+void prepare_probes(ProbeSet& ps) {
+  int idx[kMaxProbes];
+  int nn = 0, nf = 0;
+  for (int j = 0; j < ps.T; ++j)
+    if (ps.t[j] != ps.t[j]) ps.pos[j] = nn++;
+  for (int j = 0; j < ps.T; ++j)
+    if (ps.t[j] == ps.t[j]) idx[nf++] = j;
+  std::sort(idx, idx + nf, [&](int a, int b) { return ps.t[a] < ps.t[b]; });
+  const double qnan = std::numeric_limits<double>::quiet_NaN();
+  for (int k = 0; k < 16; ++k) ps.s[k] = k < nf ? ps.t[idx[k]] : qnan;
+  for (int k = 0; k < nf; ++k) ps.pos[idx[k]] = nn + k;
+  ps.nan_cnt = nn;
+}
+
 void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
                        const double* err, const uint8_t* flag, double* part, int64_t* cnt) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
-  k_probe_multi<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, ts, est, err, flag,
-                                                                       part, cnt);
+  k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
+                                                                        flag, part, cnt);
 }
 
 void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
                            const int64_t* cnt, double* scratch, ProbeScalars* out) {
-  k_finalize_multi<<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out);
+  finalize_multi(st, nblk, T, part, cnt, scratch, out);
 }
 
 void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
@@ -735,9 +923,9 @@ void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const do
                         double* scratch, ProbeScalars* out) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
-  k_probe_multi<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, ts, est, err, flag,
-                                                                       part, cnt);
-  k_finalize_multi<<<3 * ts.T, 256, 0, st>>>(nblk, ts.T, part, cnt, scratch, out);
+  k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
+                                                                        flag, part, cnt);
+  finalize_multi(st, nblk, ts.T, part, cnt, scratch, out);
 }
 
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets) {
@@ -759,7 +947,17 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
                      const unsigned long long* mm, const double* err0) {
-  k_finalize<<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm, err0);
+  const size_t sm = tree_smem_bytes(nblk, 4);
+  if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
+    // opt in to > 48 KB dynamic shared memory (per device; cheap host call)
+    cudaFuncSetAttribute(k_finalize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kTreeSmemMaxBytes));
+    k_finalize<true><<<1, kFinThreads, sm, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
+                                                 err0);
+  } else {
+    k_finalize<false><<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
+                                                 err0);
+  }
 }
 
 void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,

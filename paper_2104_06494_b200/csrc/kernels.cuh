@@ -29,9 +29,18 @@ struct FoldScalars {
 constexpr int kMaxProbes = 15;
 struct ProbeSet {
   int T;
-  int pad;
-  double t[kMaxProbes];
+  int nan_cnt;           // thresholds that are NaN (they occupy sorted positions 0..nan_cnt-1)
+  double t[kMaxProbes];  // tree order (node j)
+  // Filled by prepare_probes(): finite thresholds ascending, NaN-padded to 16,
+  // and the sorted position of every node.  A region's code is
+  // flag ? (err NaN ? 16 : nan_cnt + #{s_k <= err}) : 0, and it is a
+  // candidate of node j  <=>  code > pos[j]  <=>  flag && !(err < t[j]).
+  double s[16];
+  int pos[kMaxProbes];
+  int pad2;
 };
+// Host: sort the node thresholds into ps.s / ps.pos / ps.nan_cnt.
+void prepare_probes(ProbeSet& ps);
 struct ProbeScalars {
   double err_sum[kMaxProbes];  // sum err where candidate == 0 (discarded)
   double est_sum[kMaxProbes];  // sum est where candidate == 0
