@@ -563,7 +563,9 @@ def glibc_exp(x, on_device=True):
 
 
 def glibc_cos(x, on_device=True, branch_free=False):
-    """glibc cos restatement; branch_free selects the SIMT variant used by f1."""
+    """glibc cos restatement.  on_device: the evaluator's device variant (the
+    one f1 uses); branch_free: the branch-merged SIMT variant (kept as an
+    alternative, measured slower on B200)."""
     x = _f64(x)
     y = np.empty_like(x)
     code = (2 if on_device else 3) if branch_free else int(bool(on_device))

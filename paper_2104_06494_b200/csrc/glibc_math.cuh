@@ -194,16 +194,37 @@ PGN_HD double gm_exp_k(double x, const uint64_t* __restrict__ T, const ExpK& K) 
 
 // ---- cos: sysdeps/ieee754/dbl-64/s_sin.c (glibc 2.39), __cos_fma ---------
 
+// The non-immediate cos constants of the hot path as values (see ExpK):
+// hoisted into registers by the evaluator (PGN_HOIST_COS), immediates otherwise.
+struct CosK {
+  double hpinv = pgn_asf64(cosc::kHpinv);
+  double mp1 = pgn_asf64(cosc::kMp1);
+  double mp2 = pgn_asf64(cosc::kMp2);
+  double pp3 = pgn_asf64(cosc::kPp3);
+  double pp4 = pgn_asf64(cosc::kPp4);
+  double sn3 = pgn_asf64(cosc::kSn3);
+  double sn5 = pgn_asf64(cosc::kSn5);
+  double cs4 = pgn_asf64(cosc::kCs4);
+  double cs6 = pgn_asf64(cosc::kCs6);
+  double s1 = pgn_asf64(cosc::kS1);  // TAYLOR_SIN
+  double s2 = pgn_asf64(cosc::kS2);
+  double s3 = pgn_asf64(cosc::kS3);
+  double s4 = pgn_asf64(cosc::kS4);
+  double s5 = pgn_asf64(cosc::kS5);
+  double taylor_max = pgn_asf64(cosc::kTaylorMax);
+};
+
 // s_sin.c do_cos(x, dx)
-PGN_HD double gm_do_cos(double x, double dx, const double* __restrict__ SC) {
+PGN_HD double gm_do_cos(double x, double dx, const double* __restrict__ SC,
+                         const CosK& KC = CosK{}) {
   if (x < 0) dx = -dx;
   const double ax = pgn_fabs(x);
   const double u = P_ADD(PGN_C(kBig), ax);
   const double xr = P_ADD(P_SUB(ax, P_SUB(u, PGN_C(kBig))), dx);
   const double xx = P_MUL(xr, xr);
-  const double s = P_FMA(P_MUL(xr, xx), P_FMA(xx, PGN_C(kSn5), PGN_C(kSn3)), xr);
+  const double s = P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), xr);
   const double c =
-      P_MUL(xx, P_FMA(xx, P_FMA(xx, PGN_C(kCs6), PGN_C(kCs4)), PGN_C(kCs2)));
+      P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2)));
   const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
   const double sn = SC[k], ssn = SC[k + 1], cs = SC[k + 2], ccs = SC[k + 3];
   double cor = P_FMA(-s, ssn, ccs);
@@ -213,7 +234,8 @@ PGN_HD double gm_do_cos(double x, double dx, const double* __restrict__ SC) {
 }
 
 // s_sin.c do_sin(x, dx), including the TAYLOR_SIN branch.
-PGN_HD double gm_do_sin(double x, double dx, const double* __restrict__ SC) {
+PGN_HD double gm_do_sin(double x, double dx, const double* __restrict__ SC,
+                         const CosK& KC = CosK{}) {
   if (pgn_fabs(x) < PGN_C(kTaylorMax)) {
     const double xx = P_MUL(x, x);
     double p = P_FMA(PGN_C(kS5), xx, PGN_C(kS4));
@@ -229,9 +251,9 @@ PGN_HD double gm_do_sin(double x, double dx, const double* __restrict__ SC) {
   const double u = P_ADD(PGN_C(kBig), ax);
   const double xr = P_SUB(ax, P_SUB(u, PGN_C(kBig)));
   const double xx = P_MUL(xr, xr);
-  const double s = P_ADD(xr, P_FMA(P_MUL(xr, xx), P_FMA(xx, PGN_C(kSn5), PGN_C(kSn3)), dx));
+  const double s = P_ADD(xr, P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), dx));
   const double c = P_FMA(
-      xr, dx, P_MUL(xx, P_FMA(xx, P_FMA(xx, PGN_C(kCs6), PGN_C(kCs4)), PGN_C(kCs2))));
+      xr, dx, P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2))));
   const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
   const double sn = SC[k], ssn = SC[k + 1], cs = SC[k + 2], ccs = SC[k + 3];
   double cor = P_FMA(s, ccs, ssn);
@@ -249,26 +271,26 @@ PGN_HD bool gm_cos_in_range(double x) {
   return k < 0x419921fbu;
 }
 
-PGN_HD double gm_cos(double x, const double* __restrict__ SC) {
+PGN_HD double gm_cos(double x, const double* __restrict__ SC, const CosK& KC = CosK{}) {
   const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e400000u) return 1.0;          // |x| < 2^-27
-  if (k < 0x3feb6000u) return gm_do_cos(x, 0.0, SC);  // |x| < 0.855469
+  if (k < 0x3feb6000u) return gm_do_cos(x, 0.0, SC, KC);  // |x| < 0.855469
   if (k < 0x400368fdu) {                     // |x| < 2.426265
     const double y = P_SUB(PGN_C(kHp0), pgn_fabs(x));
     const double a = P_ADD(y, PGN_C(kHp1));
     const double da = P_ADD(P_SUB(y, a), PGN_C(kHp1));
-    return gm_do_sin(a, da, SC);
+    return gm_do_sin(a, da, SC, KC);
   }
   if (k < 0x419921fbu) {                     // |x| < 105414350: reduce_sincos
-    const double t = P_FMA(x, PGN_C(kHpinv), PGN_C(kToint));
+    const double t = P_FMA(x, KC.hpinv, PGN_C(kToint));
     const double xn = P_SUB(t, PGN_C(kToint));
     const int n = static_cast<int>(pgn_asu64(t) & 3);
-    const double y = P_FMA(-xn, PGN_C(kMp2), P_FMA(-xn, PGN_C(kMp1), x));
-    const double t2 = P_FMA(-xn, PGN_C(kPp3), y);
-    double db = P_FMA(-xn, PGN_C(kPp3), P_SUB(y, t2));
-    const double b = P_FMA(-xn, PGN_C(kPp4), t2);
-    db = P_ADD(db, P_FMA(-xn, PGN_C(kPp4), P_SUB(t2, b)));
-    const double r = (n & 1) ? gm_do_sin(b, db, SC) : gm_do_cos(b, db, SC);
+    const double y = P_FMA(-xn, KC.mp2, P_FMA(-xn, KC.mp1, x));
+    const double t2 = P_FMA(-xn, KC.pp3, y);
+    double db = P_FMA(-xn, KC.pp3, P_SUB(y, t2));
+    const double b = P_FMA(-xn, KC.pp4, t2);
+    db = P_ADD(db, P_FMA(-xn, KC.pp4, P_SUB(t2, b)));
+    const double r = (n & 1) ? gm_do_sin(b, db, SC, KC) : gm_do_cos(b, db, SC, KC);
     return ((n + 1) & 2) ? -r : r;
   }
   if (k < 0x7ff00000u) {
@@ -354,6 +376,148 @@ PGN_HD double gm_cos_bf(double x, const double* __restrict__ SC) {
   if (k >= 0x419921fbu) r = gm_cos(x, SC);
   return r;
 }
+
+// ---------------------------------------------------------------------------
+// Device hot-path variants (same arithmetic, bit-identical results; checked
+// against gm_exp / gm_cos and libm by the tests).  Differences are in the
+// instructions around the arithmetic only:
+//  * the tables are read with 32-bit shared-memory addresses computed once per
+//    kernel (a generic pointer made ptxas rebuild the shared window base --
+//    S2UR + ULEA + LEA -- on every call);
+//  * `-v` and copysign are sign-bit XORs (what gcc emits for the reference on
+//    x86: xorpd), instead of an FP64 DADD(-0, -v) plus two FSELs;
+//  * gm_cos tests the common range (2.43 <= |x| < 1.05e8, reduce_sincos)
+//    first.
+PGN_HD double pgn_xor_sign(double v, bool c) {
+  return pgn_asf64(pgn_asu64(v) ^ (static_cast<uint64_t>(c) << 63));
+}
+
+#if defined(__CUDACC__)
+struct SmemTab {  // a table in shared memory, by 32-bit shared address
+  uint32_t a;
+  __device__ __forceinline__ void ld2(int i, double& x, double& y) const {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + 8u * i));
+  }
+  __device__ __forceinline__ void ld2u(int i, uint64_t& x, uint64_t& y) const {
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a + 8u * i));
+  }
+};
+
+__device__ __forceinline__ double gm_exp_s(double x, SmemTab T, const ExpK& K) {
+  using namespace expc;
+  const uint64_t ix = pgn_asu64(x);
+  uint32_t abstop = static_cast<uint32_t>(ix >> 52) & 0x7ff;
+  if (abstop - 0x3c9u >= 0x3fu) {
+    if (static_cast<int32_t>(abstop - 0x3c9u) < 0) return P_ADD(1.0, x);  // |x| < 2^-54
+    if (abstop >= 0x409u) {                                               // |x| >= 1024
+      if (ix == 0xfff0000000000000ULL) return 0.0;
+      if (abstop >= 0x7ffu) return P_ADD(1.0, x);
+      if (ix >> 63) return 0.0;                          // __math_uflow(0)
+      return pgn_asf64(0x7ff0000000000000ULL);           // __math_oflow(0)
+    }
+    abstop = 0;  // large |x|: handled by the special case below
+  }
+  double kd = P_FMA(x, K.inv_ln2_n, PGN_GM(expc, kShift));
+  const uint64_t ki = pgn_asu64(kd);
+  kd = P_SUB(kd, PGN_GM(expc, kShift));
+  double r = P_FMA(kd, K.neg_ln2hi_n, x);
+  r = P_FMA(kd, K.neg_ln2lo_n, r);
+  const int idx = 2 * static_cast<int>(ki & 127);
+  const uint64_t top = ki << 45;
+  uint64_t tail_b, sb;
+  T.ld2u(idx, tail_b, sb);
+  const double tail = pgn_asf64(tail_b);
+  const uint64_t sbits = sb + top;
+  const double p23 = P_FMA(r, K.c3, K.c2);
+  const double tr = P_ADD(r, tail);
+  const double r2 = P_MUL(r, r);
+  const double p45 = P_FMA(r, K.c5, K.c4);
+  const double t = P_FMA(p23, r2, tr);
+  const double r4 = P_MUL(r2, r2);
+  const double tmp = P_FMA(r4, p45, t);
+  if (abstop == 0) return gm_exp_special(tmp, sbits, ki);
+  const double scale = pgn_asf64(sbits);
+  return P_FMA(scale, tmp, scale);
+}
+
+__device__ __forceinline__ void gm_sc4(SmemTab SC, int k, double& sn, double& ssn, double& cs,
+                                       double& ccs) {
+  SC.ld2(k, sn, ssn);
+  SC.ld2(k + 2, cs, ccs);
+}
+
+__device__ __forceinline__ double gm_do_cos_s(double x, double dx, SmemTab SC, const CosK& KC) {
+  dx = pgn_xor_sign(dx, x < 0);
+  const double ax = pgn_fabs(x);
+  const double u = P_ADD(PGN_C(kBig), ax);
+  const double xr = P_ADD(P_SUB(ax, P_SUB(u, PGN_C(kBig))), dx);
+  const double xx = P_MUL(xr, xr);
+  const double s = P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), xr);
+  const double c = P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2)));
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  double sn, ssn, cs, ccs;
+  gm_sc4(SC, k, sn, ssn, cs, ccs);
+  double cor = P_FMA(-s, ssn, ccs);
+  cor = P_FMA(-c, cs, cor);
+  cor = P_FMA(-s, sn, cor);
+  return P_ADD(cs, cor);
+}
+
+__device__ __forceinline__ double gm_do_sin_s(double x, double dx, SmemTab SC, const CosK& KC) {
+  if (pgn_fabs(x) < KC.taylor_max) {
+    const double xx = P_MUL(x, x);
+    double p = P_FMA(KC.s5, xx, KC.s4);
+    p = P_FMA(p, xx, KC.s3);
+    p = P_FMA(p, xx, KC.s2);
+    p = P_FMA(p, xx, KC.s1);
+    const double t = P_FMA(xx, P_FMA(p, x, -P_MUL(0.5, dx)), dx);
+    return P_ADD(x, t);
+  }
+  const uint64_t xsign = pgn_asu64(x) & 0x8000000000000000ULL;
+  dx = pgn_xor_sign(dx, x <= 0);
+  const double ax = pgn_fabs(x);
+  const double u = P_ADD(PGN_C(kBig), ax);
+  const double xr = P_SUB(ax, P_SUB(u, PGN_C(kBig)));
+  const double xx = P_MUL(xr, xr);
+  const double s = P_ADD(xr, P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), dx));
+  const double c =
+      P_FMA(xr, dx, P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2))));
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  double sn, ssn, cs, ccs;
+  gm_sc4(SC, k, sn, ssn, cs, ccs);
+  double cor = P_FMA(s, ccs, ssn);
+  cor = P_FMA(-c, sn, cor);
+  cor = P_FMA(s, cs, cor);
+  const double r = P_ADD(sn, cor);
+  return pgn_asf64((pgn_asu64(r) & 0x7fffffffffffffffULL) | xsign);
+}
+
+__device__ __forceinline__ double gm_cos_s(double x, SmemTab SC, const CosK& KC) {
+  const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
+  if (k - 0x400368fdu < 0x419921fbu - 0x400368fdu) {  // 2.426265 <= |x| < 105414350
+    const double t = P_FMA(x, KC.hpinv, PGN_C(kToint));
+    const double xn = P_SUB(t, PGN_C(kToint));
+    const int n = static_cast<int>(pgn_asu64(t) & 3);
+    const double y = P_FMA(-xn, KC.mp2, P_FMA(-xn, KC.mp1, x));
+    const double t2 = P_FMA(-xn, KC.pp3, y);
+    double db = P_FMA(-xn, KC.pp3, P_SUB(y, t2));
+    const double b = P_FMA(-xn, KC.pp4, t2);
+    db = P_ADD(db, P_FMA(-xn, KC.pp4, P_SUB(t2, b)));
+    const double r = (n & 1) ? gm_do_sin_s(b, db, SC, KC) : gm_do_cos_s(b, db, SC, KC);
+    return pgn_xor_sign(r, ((n + 1) & 2) != 0);
+  }
+  if (k < 0x3e400000u) return 1.0;                         // |x| < 2^-27
+  if (k < 0x3feb6000u) return gm_do_cos_s(x, 0.0, SC, KC);  // |x| < 0.855469
+  if (k < 0x400368fdu) {                                   // |x| < 2.426265
+    const double y = P_SUB(PGN_C(kHp0), pgn_fabs(x));
+    const double a = P_ADD(y, PGN_C(kHp1));
+    const double da = P_ADD(P_SUB(y, a), PGN_C(kHp1));
+    return gm_do_sin_s(a, da, SC, KC);
+  }
+  if (k < 0x7ff00000u) return ::cos(x);  // __branred territory: not restated
+  return P_DIV(x, x);                    // inf or nan -> nan
+}
+#endif  // __CUDACC__
 
 #undef PGN_C
 

@@ -29,7 +29,35 @@ struct MathTables {
   const uint64_t* exp_tab;  // 256 u64 (glibc __exp_data.tab)
   const double* sincos;     // 440 doubles (glibc __sincostab)
   ExpK K{};                 // exp constants (immediates unless the kernel hoists them)
+  CosK KC{};                // cos constants (likewise)
+  uint32_t exp_s = 0, sc_s = 0;  // shared-memory addresses of the two tables (device)
 };
+
+#if defined(__CUDACC__)
+// Device tables: both tables live in shared memory.
+__device__ __forceinline__ MathTables make_tables(const uint64_t* s_exp, const double* s_sc) {
+  MathTables T{s_exp, s_sc};
+  T.exp_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_exp));
+  T.sc_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_sc));
+  return T;
+}
+#endif
+
+// exp / cos of the hot path: shared-address variants on the device.
+PGN_HD double tab_exp(double x, const MathTables& T) {
+#if defined(__CUDA_ARCH__)
+  return gm_exp_s(x, SmemTab{T.exp_s}, T.K);
+#else
+  return gm_exp_k(x, T.exp_tab, T.K);
+#endif
+}
+PGN_HD double tab_cos(double x, const MathTables& T) {
+#if defined(__CUDA_ARCH__)
+  return gm_cos_s(x, SmemTab{T.sc_s}, T.KC);
+#else
+  return gm_cos(x, T.sincos, T.KC);
+#endif
+}
 
 struct IntegrandParams {
   double p[32];
@@ -51,6 +79,7 @@ PGN_HD double ipow(double base, int e) {
 
 struct F1 {  // cos(sum (i+1) x_i)              integrands.cpp:24-28
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 2;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 1), x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
@@ -58,7 +87,7 @@ struct F1 {  // cos(sum (i+1) x_i)              integrands.cpp:24-28
 #if PGN_F1_COS_BF
     return gm_cos_bf(s, T.sincos);
 #else
-    return gm_cos(s, T.sincos);
+    return tab_cos(s, T);
 #endif
   }
   PGN_HD static bool cut(int, double) { return false; }
@@ -66,6 +95,7 @@ struct F1 {  // cos(sum (i+1) x_i)              integrands.cpp:24-28
 
 struct F2 {  // prod 1/(1/2500 + (x-1/2)^2)      integrands.cpp:30-37
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 0;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 1.0; }
   PGN_HD static double term(int, double x) {
     const double t = P_SUB(x, 0.5);
@@ -78,6 +108,7 @@ struct F2 {  // prod 1/(1/2500 + (x-1/2)^2)      integrands.cpp:30-37
 
 struct F3 {  // (1 + sum (i+1) x_i)^-(n+1)       integrands.cpp:39-43
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 0;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 1.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 1), x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
@@ -89,6 +120,7 @@ struct F3 {  // (1 + sum (i+1) x_i)^-(n+1)       integrands.cpp:39-43
 
 struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 1;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int, double x) {
     const double t = P_SUB(x, 0.5);
@@ -96,29 +128,31 @@ struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
-    return gm_exp_k(P_MUL(-625.0, s), T.exp_tab, T.K);
+    return tab_exp(P_MUL(-625.0, s), T);
   }
   PGN_HD static bool cut(int, double) { return false; }
 };
 
 struct F5 {  // exp(-10 sum |x-1/2|)             integrands.cpp:54-58
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 1;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int, double x) { return pgn_fabs(P_SUB(x, 0.5)); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
-    return gm_exp_k(P_MUL(-10.0, s), T.exp_tab, T.K);
+    return tab_exp(P_MUL(-10.0, s), T);
   }
   PGN_HD static bool cut(int, double) { return false; }
 };
 
 struct F6 {  // exp(sum (i+5) x_i), 0 outside    integrands.cpp:60-67
   static constexpr bool kSeparable = true, kCut = true;
+  static constexpr int kMath = 1;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 5), x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
-    return gm_exp_k(s, T.exp_tab, T.K);
+    return tab_exp(s, T);
   }
   PGN_HD static bool cut(int a, double x) {
     return x >= P_DIV(P_ADD(3.0, static_cast<double>(a + 1)), 10.0);
@@ -127,6 +161,7 @@ struct F6 {  // exp(sum (i+5) x_i), 0 outside    integrands.cpp:60-67
 
 struct F7 {  // (sum x^2)^11                     integrands.cpp:69-73
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 0;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int, double x) { return P_MUL(x, x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
@@ -136,6 +171,7 @@ struct F7 {  // (sum x^2)^11                     integrands.cpp:69-73
 
 struct F8 {  // (sum x^2)^7 sqrt(sum x^2)        integrands.cpp:75-79
   static constexpr bool kSeparable = true, kCut = false;
+  static constexpr int kMath = 0;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int, double x) { return P_MUL(x, x); }
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }

@@ -711,7 +711,10 @@ __global__ void k_math(int which, int64_t m, const double* x, double* y) {
   load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  y[j] = which == 0 ? gm_exp(x[j], s_exp) : (which == 1 ? gm_cos(x[j], s_sc) : gm_cos_bf(x[j], s_sc));
+  // the evaluator's hot-path variants (tab_exp / tab_cos: shared-address
+  // tables, sign-bit XORs) and the branch-free cos
+  const MathTables T = make_tables(s_exp, s_sc);
+  y[j] = which == 0 ? tab_exp(x[j], T) : (which == 1 ? tab_cos(x[j], T) : gm_cos_bf(x[j], s_sc));
 }
 
 template <class F>
@@ -721,7 +724,7 @@ __global__ void k_call(int n, int64_t m, const double* x, IntegrandParams ip, do
   load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
-  const MathTables T{s_exp, s_sc};
+  const MathTables T = make_tables(s_exp, s_sc);
   double xx[16];
   for (int a = 0; a < n; ++a) xx[a] = x[j * n + a];
   y[j] = eval_point<F>(xx, n, ip, T);
