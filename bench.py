@@ -112,6 +112,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def measured_hbm_peak():
+    """HBM copy bandwidth from the driver-written MEASURED_PEAKS.json (GB/s)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "of measured: MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "of fallback: 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
 # --------------------------------------------------------------- ours -------
 def run_ours(args, rank, world, local_rank):
     import paper_2104_06494_b200 as pg
@@ -211,6 +220,19 @@ def run_ours(args, rank, world, local_rank):
                          "it": r.iterations, "regions": r.regions_generated,
                          "estimate": r.estimate, "time_to_result_s": r.device_ms / 1e3})
     achieved = flops / (eval_ms / 1e3) / 1e12 if eval_ms > 0 else 0.0
+    # HBM rooflines of the memory-side kernels: algorithmic bytes (DESIGN.md 4,
+    # counted by the driver per launch) / their CUDA-event time.
+    hbm_peak, hbm_src = measured_hbm_peak()
+    hbm = {}
+    for k, label in (("split", "k_split (filter + bisect)"),
+                     ("probe", "k_probe_multi + trees (threshold classify)")):
+        ms = sum(r.kernel_ms[k] for st in steps for _, _, r in st)
+        by = sum(r.kernel_bytes[k] for st in steps for _, _, r in st)
+        if ms > 0:
+            gbs = by / (ms / 1e3) / 1e9
+            hbm[k] = {"kernel": label, "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": gbs / hbm_peak if hbm_peak else None,
+                      "bytes_per_step": by / args.steps, "ms_per_step": ms / args.steps}
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_evaluate_summary.json")
     if os.path.exists(prof_path):
@@ -245,6 +267,7 @@ def run_ours(args, rank, world, local_rank):
                                                          for _, _, r in st) / args.steps, 3)
                                             for k in ("evaluate", "fold", "finalize", "minmax",
                                                       "probe", "split", "init")}},
+        "hbm_rooflines": {"peak_source": hbm_src, **hbm},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,

@@ -31,7 +31,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define PAGANI_ABI_VERSION 1
+#define PAGANI_ABI_VERSION 2
 
 #define PAGANI_OK 0
 #define PAGANI_E_INVALID (-1)
@@ -164,6 +164,9 @@ typedef struct pagani_result {
   int64_t peak_regions;
   int64_t h2d_bytes, d2h_bytes;
   double device_ms; /* CUDA-event span on the driver stream: first kernel -> last */
+  /* Algorithmic HBM bytes per kernel kind (what each launch must read and
+   * write), for the HBM rooflines of the memory kernels. */
+  double kernel_bytes[PAGANI_N_KERNEL_SLOTS];
 } pagani_result;
 
 /* One row per iteration (the BFCUB_TRACE point, driver.cpp:174-182, in full

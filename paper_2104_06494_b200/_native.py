@@ -90,7 +90,8 @@ class Result(C.Structure):
                 ("kernel_launches", C.c_int64 * PAGANI_N_KERNEL_SLOTS),
                 ("region_evals", C.c_int64), ("peak_regions", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("device_ms", C.c_double)]
+                ("device_ms", C.c_double),
+                ("kernel_bytes", C.c_double * PAGANI_N_KERNEL_SLOTS)]
 
 
 class ThresholdResult(C.Structure):

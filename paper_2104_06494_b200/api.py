@@ -186,6 +186,7 @@ class IntegrationResult:
     wall_ms: float = 0.0
     kernel_ms: dict = field(default_factory=dict)
     kernel_launches: dict = field(default_factory=dict)
+    kernel_bytes: dict = field(default_factory=dict)  # algorithmic HBM bytes per kernel kind
     region_evals: int = 0
     peak_regions: int = 0
     h2d_bytes: int = 0
@@ -306,6 +307,7 @@ def integrate(f, bounds: Bounds, config: Optional[Config] = None,
         eval_count=out.eval_count, threshold_events=events, wall_ms=out.wall_ms,
         kernel_ms={k: out.kernel_ms[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         kernel_launches={k: out.kernel_launches[i] for i, k in enumerate(N.KERNEL_SLOTS)},
+        kernel_bytes={k: out.kernel_bytes[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         region_evals=out.region_evals, peak_regions=out.peak_regions,
         h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, device_ms=out.device_ms,
         trace=rows if trace else None)

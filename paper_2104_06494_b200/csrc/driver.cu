@@ -583,6 +583,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     const size_t k1 = kt.mark();
     kt.span(PAGANI_K_EVALUATE, k0, k1);
     out->kernel_launches[PAGANI_K_EVALUATE] += m > 0;
+    // reads low/len (16n) [+ pest 8], writes est, err (16) + flag, axis (2)
+    out->kernel_bytes[PAGANI_K_EVALUATE] += static_cast<double>(m) * (16.0 * n + (ep.refine ? 8 : 0) + 18);
     out->eval_count += M * rule.point_count;
     out->region_evals += m;
 
@@ -673,6 +675,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
           ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, M,
           cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr, sh);
       out->kernel_ms[PAGANI_K_PROBE] += pms;
+      out->kernel_bytes[PAGANI_K_PROBE] += static_cast<double>(tr.passes) * m * 17.0;  // flag, err, est
       out->kernel_launches[PAGANI_K_PROBE] += (sh ? 5 : 2) * tr.passes + (tr.success ? 1 : 0);
       out->kernel_launches[PAGANI_K_MINMAX] += tr.minmax_launches;
       out->d2h_bytes += tr.passes * sizeof(ProbeScalars);
@@ -755,6 +758,12 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
     // ---- fused filter + bisect (+ the exchange that re-balances the shards) ---
     const size_t k4 = kt.mark();
+    {  // flag (+ err under a threshold) for every region; est, axis, low, len of
+       // each kept one; two children (low, len, parent est) per kept region.
+      const double kl = sh ? static_cast<double>(kb[rank + 1] - kb[rank]) : static_cast<double>(kept);
+      out->kernel_bytes[PAGANI_K_SPLIT] += static_cast<double>(m) * (use_t ? 9.0 : 1.0) +
+                                           kl * (16.0 * n + 9.0) + 2.0 * kl * (16.0 * n + 8.0);
+    }
     if (!sh) {
       launch_split(st, n, m, cap, cap, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p,
                    ws.err.p, ws.axis.p, ws.low[cur].p, ws.len[cur].p, ws.low[cur ^ 1].p,

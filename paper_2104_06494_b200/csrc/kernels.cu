@@ -974,6 +974,88 @@ void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long lo
   k_minmax_done<<<1, 1, 0, st>>>(m, x, keys, out);
 }
 
+// k_split_n<N>: the same fused filter + bisect as k_split with the dimension
+// known at compile time, restructured for memory-level parallelism: every
+// flag (and err) of the CTA's 8 rounds is loaded up front, the 8 rounds' ranks
+// come from one shared-memory scan (one barrier instead of 16), and each kept
+// region issues all 2N + 2 of its loads before any store.
+template <int N>
+__global__ void __launch_bounds__(kSplitThreads)
+    k_split_n(int64_t m, int64_t cap_src, int64_t cap_dst, const uint8_t* __restrict__ flag,
+              int use_t, double t, const int64_t* __restrict__ offsets,
+              const double* __restrict__ est, const double* __restrict__ err,
+              const uint8_t* __restrict__ axis, const double* __restrict__ low,
+              const double* __restrict__ len, double* __restrict__ dlow,
+              double* __restrict__ dlen, double* __restrict__ dpest, double* __restrict__ dperr,
+              int64_t kbase) {
+  constexpr int W = kSplitThreads / 32;
+  __shared__ int s_cnt[kSplitPer][W];
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlock;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool keep[kSplitPer];
+  uint8_t fl[kSplitPer];
+  double ev[kSplitPer];
+#pragma unroll
+  for (int r = 0; r < kSplitPer; ++r) {
+    const int64_t j = base + r * kSplitThreads + threadIdx.x;
+    fl[r] = j < m ? (flag ? __ldg(flag + j) : uint8_t{1}) : uint8_t{0};
+    ev[r] = (use_t && j < m) ? __ldg(err + j) : 0.0;
+  }
+  unsigned before[kSplitPer];
+#pragma unroll
+  for (int r = 0; r < kSplitPer; ++r) {
+    keep[r] = fl[r] != 0 && !(use_t && ev[r] < t);  // accepted threshold (classify.cpp:63-66)
+    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
+    before[r] = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_cnt[r][wid] = __popc(bal);
+  }
+  __syncthreads();
+  int64_t run = offsets ? offsets[b] : base;  // rank of the block's first kept region
+#pragma unroll
+  for (int r = 0; r < kSplitPer; ++r) {
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int c = s_cnt[r][w];
+      wbase += w < wid ? c : 0;
+      total += c;
+    }
+    const int64_t k = run + wbase + before[r];
+    run += total;
+    if (!keep[r]) continue;
+    const int64_t j = base + r * kSplitThreads + threadIdx.x;
+    const int ax = __ldg(axis + j);
+    const double e = __ldg(est + j);
+    double lo[N], ln[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      lo[a] = __ldg(low + a * cap_src + j);
+      ln[a] = __ldg(len + a * cap_src + j);
+    }
+    const int64_t c0 = 2 * (k - kbase);
+#pragma unroll
+    for (int a = 0; a < N; ++a) {  // geometry.cpp:122-141
+      double2 cl, cn;
+      if (a == ax) {
+        const double half = P_MUL(ln[a], 0.5);
+        cl = make_double2(lo[a], P_ADD(lo[a], half));
+        cn = make_double2(half, half);
+      } else {
+        cl = make_double2(lo[a], lo[a]);
+        cn = make_double2(ln[a], ln[a]);
+      }
+      *reinterpret_cast<double2*>(dlow + a * cap_dst + c0) = cl;
+      *reinterpret_cast<double2*>(dlen + a * cap_dst + c0) = cn;
+    }
+    *reinterpret_cast<double2*>(dpest + c0) = make_double2(e, e);
+    if (dperr) {
+      const double r2 = __ldg(err + j);
+      *reinterpret_cast<double2*>(dperr + c0) = make_double2(r2, r2);
+    }
+  }
+}
+
 void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
@@ -981,9 +1063,23 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                   double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
-  k_split<<<static_cast<unsigned>(nblk), kSplitThreads, 0, st>>>(
-      n, m, cap_src, cap_dst, flag, use_t, t, offsets, est, err, axis, low, len, dlow, dlen,
-      dpest, dperr, kbase);
+  const unsigned g = static_cast<unsigned>(nblk);
+  switch (n) {
+#define PGN_SPLIT_CASE(NN)                                                                      \
+  case NN:                                                                                      \
+    k_split_n<NN><<<g, kSplitThreads, 0, st>>>(m, cap_src, cap_dst, flag, use_t, t, offsets, est, \
+                                               err, axis, low, len, dlow, dlen, dpest, dperr,    \
+                                               kbase);                                          \
+    return;
+    PGN_SPLIT_CASE(1) PGN_SPLIT_CASE(2) PGN_SPLIT_CASE(3) PGN_SPLIT_CASE(4) PGN_SPLIT_CASE(5)
+    PGN_SPLIT_CASE(6) PGN_SPLIT_CASE(7) PGN_SPLIT_CASE(8) PGN_SPLIT_CASE(9) PGN_SPLIT_CASE(10)
+    PGN_SPLIT_CASE(11) PGN_SPLIT_CASE(12) PGN_SPLIT_CASE(13) PGN_SPLIT_CASE(14)
+    PGN_SPLIT_CASE(15) PGN_SPLIT_CASE(16)
+#undef PGN_SPLIT_CASE
+    default:
+      k_split<<<g, kSplitThreads, 0, st>>>(n, m, cap_src, cap_dst, flag, use_t, t, offsets, est,
+                                           err, axis, low, len, dlow, dlen, dpest, dperr, kbase);
+  }
 }
 
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
