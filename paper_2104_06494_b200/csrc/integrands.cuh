@@ -22,6 +22,9 @@
 #ifndef PGN_F1_COS_BF
 #define PGN_F1_COS_BF 0
 #endif
+#ifndef PGN_F1_PAIR
+#define PGN_F1_PAIR 1  // paired cos reductions: f1 k_evaluate -5% on B200
+#endif
 
 namespace pgn {
 
@@ -49,6 +52,22 @@ PGN_HD double tab_exp(double x, const MathTables& T) {
   return gm_exp_s(x, SmemTab{T.exp_s}, T.K);
 #else
   return gm_exp_k(x, T.exp_tab, T.K);
+#endif
+}
+PGN_HD void tab_exp2(double x0, double x1, const MathTables& T, double& y0, double& y1) {
+#if defined(__CUDA_ARCH__)
+  gm_exp2_s(x0, x1, SmemTab{T.exp_s}, T.K, y0, y1);
+#else
+  y0 = gm_exp_k(x0, T.exp_tab, T.K);
+  y1 = gm_exp_k(x1, T.exp_tab, T.K);
+#endif
+}
+PGN_HD void tab_cos2(double x0, double x1, const MathTables& T, double& y0, double& y1) {
+#if defined(__CUDA_ARCH__)
+  gm_cos2_s(x0, x1, SmemTab{T.sc_s}, T.KC, y0, y1);
+#else
+  y0 = gm_cos(x0, T.sincos, T.KC);
+  y1 = gm_cos(x1, T.sincos, T.KC);
 #endif
 }
 PGN_HD double tab_cos(double x, const MathTables& T) {
@@ -90,6 +109,11 @@ struct F1 {  // cos(sum (i+1) x_i)              integrands.cpp:24-28
     return tab_cos(s, T);
 #endif
   }
+#if !PGN_F1_COS_BF && PGN_F1_PAIR
+  PGN_HD static void fin2(double s0, double s1, int, const MathTables& T, double& f0, double& f1) {
+    tab_cos2(s0, s1, T, f0, f1);
+  }
+#endif
   PGN_HD static bool cut(int, double) { return false; }
 };
 
@@ -130,6 +154,9 @@ struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   PGN_HD static double fin(double s, int, const MathTables& T) {
     return tab_exp(P_MUL(-625.0, s), T);
   }
+  PGN_HD static void fin2(double s0, double s1, int, const MathTables& T, double& f0, double& f1) {
+    tab_exp2(P_MUL(-625.0, s0), P_MUL(-625.0, s1), T, f0, f1);
+  }
   PGN_HD static bool cut(int, double) { return false; }
 };
 
@@ -142,6 +169,9 @@ struct F5 {  // exp(-10 sum |x-1/2|)             integrands.cpp:54-58
   PGN_HD static double fin(double s, int, const MathTables& T) {
     return tab_exp(P_MUL(-10.0, s), T);
   }
+  PGN_HD static void fin2(double s0, double s1, int, const MathTables& T, double& f0, double& f1) {
+    tab_exp2(P_MUL(-10.0, s0), P_MUL(-10.0, s1), T, f0, f1);
+  }
   PGN_HD static bool cut(int, double) { return false; }
 };
 
@@ -153,6 +183,9 @@ struct F6 {  // exp(sum (i+5) x_i), 0 outside    integrands.cpp:60-67
   PGN_HD static double comb(double s, double t) { return P_ADD(s, t); }
   PGN_HD static double fin(double s, int, const MathTables& T) {
     return tab_exp(s, T);
+  }
+  PGN_HD static void fin2(double s0, double s1, int, const MathTables& T, double& f0, double& f1) {
+    tab_exp2(s0, s1, T, f0, f1);
   }
   PGN_HD static bool cut(int a, double x) {
     return x >= P_DIV(P_ADD(3.0, static_cast<double>(a + 1)), 10.0);
@@ -246,6 +279,23 @@ struct TExpSq {  // test_rule.cpp:154-189
     return s;
   }
 };
+
+// fin() of two independent points: the integrand's paired form when it has
+// one (interleaved dependency chains), else two calls.
+template <class F, class = void>
+struct HasFin2 { static constexpr bool value = false; };
+template <class F>
+struct HasFin2<F, decltype(void(&F::fin2))> { static constexpr bool value = true; };
+
+template <class F>
+PGN_HD void fin_pair(double s0, double s1, int n, const MathTables& T, double& f0, double& f1) {
+  if constexpr (HasFin2<F>::value) {
+    F::fin2(s0, s1, n, T, f0, f1);
+  } else {
+    f0 = F::fin(s0, n, T);
+    f1 = F::fin(s1, n, T);
+  }
+}
 
 // Full point evaluation of a separable integrand (used by the generic path
 // and by pagani_call_integrand).
