@@ -31,7 +31,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define PAGANI_ABI_VERSION 2
+#define PAGANI_ABI_VERSION 3
 
 #define PAGANI_OK 0
 #define PAGANI_E_INVALID (-1)
@@ -54,10 +54,31 @@ extern "C" {
  *                   PAGANI_TEST_* (tests/test_*.cpp lambdas), parameterised by
  *                   params[].
  *   PAGANI_HOST_FN: rejected with PAGANI_E_UNSUPPORTED (no CPU fallback).
+ *   PAGANI_DEVICE_FN: a user integrand compiled for the GPU by the caller
+ *                   (include/pagani_device.cuh instantiates the evaluation
+ *                   kernel for a C++ functor and fills device_fn); this is
+ *                   the device counterpart of the reference's arbitrary
+ *                   {fn, ctx} integrand (integrand.hpp:8-13).
  * `magic` must be PAGANI_INTEGRAND_MAGIC.                                     */
 #define PAGANI_INTEGRAND_MAGIC 0x50474e49u /* 'PGNI' */
 #define PAGANI_BUILTIN 0
 #define PAGANI_HOST_FN 1
+#define PAGANI_DEVICE_FN 2
+
+/* A caller-compiled evaluation kernel (PAGANI_DEVICE_FN).  `launch` runs the
+ * PAGANI evaluation of one batch of m regions on `stream` (a cudaStream_t):
+ * `params` points at the library's parameter block of `params_size` bytes,
+ * which the kernel was compiled against (a size mismatch means a header /
+ * library version mismatch and is rejected); the two table pointers are the
+ * device copies of glibc's exp / sincos tables.  Returns 0 or a cudaError_t. */
+#define PAGANI_DEVICE_FN_MAGIC 0x50474e44u /* 'PGND' */
+typedef struct pagani_device_fn {
+  uint32_t magic;
+  uint32_t params_size;
+  int (*launch)(const void* params, uint32_t params_size, const void* exp_table,
+                const void* sincos_table, void* stream, int64_t m, int32_t mode, void* user);
+  void* user;
+} pagani_device_fn;
 
 #define PAGANI_F1 1 /* cos(sum (i+1) x_i)                 integrands.cpp:24-28 */
 #define PAGANI_F2 2 /* prod 1/(1/2500 + (x_i - 1/2)^2)    integrands.cpp:30-37 */
@@ -80,12 +101,13 @@ extern "C" {
 
 typedef struct pagani_integrand {
   uint32_t magic;
-  int32_t kind;       /* PAGANI_BUILTIN | PAGANI_HOST_FN */
+  int32_t kind;       /* PAGANI_BUILTIN | PAGANI_HOST_FN | PAGANI_DEVICE_FN */
   int32_t builtin_id; /* PAGANI_F1.. / PAGANI_TEST_* */
   int32_t n_params;
   double params[PAGANI_MAX_PARAMS];
   double (*host_fn)(const double* x, int n, void* ctx); /* PAGANI_HOST_FN only */
   void* host_ctx;
+  const pagani_device_fn* device_fn; /* PAGANI_DEVICE_FN only */
 } pagani_integrand;
 
 /* ---- config (replaces bfcub::Config, driver.hpp:30-45, and ThresholdLimits,

@@ -37,7 +37,7 @@ REFINER_IDENTITY = 1
 class Integrand(C.Structure):
     _fields_ = [("magic", C.c_uint32), ("kind", C.c_int32), ("builtin_id", C.c_int32),
                 ("n_params", C.c_int32), ("params", C.c_double * PAGANI_MAX_PARAMS),
-                ("host_fn", C.c_void_p), ("host_ctx", C.c_void_p)]
+                ("host_fn", C.c_void_p), ("host_ctx", C.c_void_p), ("device_fn", C.c_void_p)]
 
 
 class TraceRow(C.Structure):

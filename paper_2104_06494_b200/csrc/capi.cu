@@ -159,8 +159,8 @@ int pagani_evaluate_batch(const pagani_integrand* f, int n, int64_t m, const dou
   return guarded([&] {
     if (n < 1 || n > 16) throw std::invalid_argument("evaluate_batch: dimension mismatch");
     const pgn::DeviceIntegrand di = pgn::resolve_integrand(f);
-    const pgn::EvalLaunch k = pgn::lookup_evaluate(di.fid, n, mode);
-    if (!k.fn) throw pgn::UnsupportedError("no device kernel for this integrand/dimension");
+    const pgn::EvalLaunch k = pgn::evaluate_kernel(di, n, mode);
+    if (!k.valid()) throw pgn::UnsupportedError("no device kernel for this integrand/dimension");
     const pgn::RuleOrbits rule = pgn::build_rule_orbits(n);
     if (eval_count) *eval_count = m * rule.point_count;
     if (m <= 0) return;

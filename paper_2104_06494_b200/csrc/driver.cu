@@ -184,6 +184,18 @@ DeviceIntegrand resolve_integrand(const pagani_integrand* f) {
     throw UnsupportedError(
         "host function-pointer integrands cannot run on the GPU (no CPU fallback); "
         "use a builtin integrand");
+  if (f->kind == PAGANI_DEVICE_FN) {
+    const pagani_device_fn* d = f->device_fn;
+    if (!d || d->magic != PAGANI_DEVICE_FN_MAGIC || !d->launch)
+      throw std::invalid_argument("integrand: PAGANI_DEVICE_FN without a valid device_fn");
+    if (d->params_size != sizeof(EvalParams))
+      throw std::invalid_argument(
+          "integrand: device_fn was compiled against a different pagani_device.cuh "
+          "(parameter block size mismatch)");
+    DeviceIntegrand di;
+    di.ext = d;
+    return di;
+  }
   if (f->kind != PAGANI_BUILTIN) throw std::invalid_argument("integrand: unknown kind");
   const int id = f->builtin_id;
   const bool ok = (id >= 1 && id <= 8) || (id >= 100 && id <= 106);
@@ -193,6 +205,16 @@ DeviceIntegrand resolve_integrand(const pagani_integrand* f) {
   const int np = f->n_params < 0 ? 0 : (f->n_params > 32 ? 32 : f->n_params);
   for (int i = 0; i < np; ++i) d.params.p[i] = f->params[i];
   return d;
+}
+
+EvalLaunch evaluate_kernel(const DeviceIntegrand& di, int n, int mode) {
+  if (di.ext) {
+    EvalLaunch k;
+    k.ext = di.ext;
+    k.mode = mode;
+    return k;
+  }
+  return lookup_evaluate(di.fid, n, mode);
 }
 
 // ---------------------------------------------------------------------------
@@ -431,8 +453,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   const DeviceIntegrand di = resolve_integrand(f);
   if (cfg.mode != PAGANI_MODE_PARITY && cfg.mode != PAGANI_MODE_FAST)
     throw std::invalid_argument("Config: unknown mode");
-  EvalLaunch eval_k = lookup_evaluate(di.fid, n, cfg.mode);
-  if (!eval_k.fn) throw UnsupportedError("no device kernel for this integrand/dimension");
+  EvalLaunch eval_k = evaluate_kernel(di, n, cfg.mode);
+  if (!eval_k.valid()) throw UnsupportedError("no device kernel for this integrand/dimension");
   if (std::getenv("PAGANI_UNFUSED_FOLD")) eval_k.fused_fold = false;  // A/B experiments
 
   // ---- ranks ------------------------------------------------------------------

@@ -100,7 +100,10 @@ void release_workspaces();
 struct DeviceIntegrand {
   int fid = 0;
   IntegrandParams params{};
+  const pagani_device_fn* ext = nullptr;  // PAGANI_DEVICE_FN
 };
+// The evaluation kernel of an integrand for dimension n and mode.
+EvalLaunch evaluate_kernel(const DeviceIntegrand& di, int n, int mode);
 DeviceIntegrand resolve_integrand(const pagani_integrand* f);
 
 struct ThresholdOutcome {

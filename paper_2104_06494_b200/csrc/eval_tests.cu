@@ -4,6 +4,7 @@
 #include <set>
 #include <utility>
 
+#include "driver.hpp"
 #include "kernels.cuh"
 
 namespace pgn {
@@ -45,6 +46,14 @@ EvalLaunch lookup_evaluate(int fid, int n, int mode) {
 }
 
 void launch_evaluate(const EvalLaunch& k, cudaStream_t st, const EvalParams& ep) {
+  if (k.ext) {  // caller-compiled kernel (include/pagani_device.cuh)
+    const int rc = k.ext->launch(&ep, static_cast<uint32_t>(sizeof(EvalParams)), device_exp_table(),
+                                 device_sincos_table(), st, ep.m, k.mode, k.ext->user);
+    if (rc != 0)
+      throw CudaError(std::string("PAGANI_DEVICE_FN launch failed: ") +
+                      cudaGetErrorString(static_cast<cudaError_t>(rc)));
+    return;
+  }
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> configured;
   int dev = 0;

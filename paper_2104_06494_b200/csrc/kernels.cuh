@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/pagani.h"
 #include "evaluate.cuh"
 
 namespace pgn {
@@ -52,6 +53,9 @@ struct EvalLaunch {
   EvalKernel fn = nullptr;
   size_t smem = 0;          // dynamic shared memory bytes
   bool fused_fold = false;  // kernel runs the 2048-block folds in its tail
+  const pagani_device_fn* ext = nullptr;  // caller-compiled kernel (PAGANI_DEVICE_FN)
+  int mode = 0;                           // for ext
+  bool valid() const { return fn != nullptr || ext != nullptr; }
 };
 
 // ---- launchers (kernels.cu) ------------------------------------------------

@@ -38,7 +38,7 @@ def test_library_loads_and_binds_all_signatures(pg):
     for name in declared_functions():
         assert name in _native.SIGNATURES, name
         assert getattr(lib, name) is not None
-    assert lib.pagani_abi_version() == 2
+    assert lib.pagani_abi_version() == 3
 
 
 def test_rule_weights_bit_identical_to_reference(pg, ref):
