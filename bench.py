@@ -215,10 +215,17 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     per_case = []
+    import importlib
+    suite = importlib.import_module("paper_2104_06494_b200.suite")  # the module, not pg.suite()
     for fid, tau, r in steps[-1]:
+        exact = suite.reference_value(f"f{fid}", DIM, corrected=True)
+        true_rel = abs(r.estimate - exact) / abs(exact) if exact else None
         per_case.append({"f": f"f{fid}", "tau": tau, "status": str(r.status),
                          "it": r.iterations, "regions": r.regions_generated,
-                         "estimate": r.estimate, "time_to_result_s": r.device_ms / 1e3})
+                         "estimate": r.estimate, "errorest": r.errorest,
+                         "true_rel_err": true_rel,
+                         "true_rel_err_le_tau": bool(true_rel is not None and true_rel <= tau),
+                         "time_to_result_s": r.device_ms / 1e3})
     achieved = flops / (eval_ms / 1e3) / 1e12 if eval_ms > 0 else 0.0
     # HBM rooflines of the memory-side kernels: algorithmic bytes (DESIGN.md 4,
     # counted by the driver per launch) / their CUDA-event time.
