@@ -1,0 +1,56 @@
+"""Run every BASELINE.json config on one GPU (time-to-tolerance, region-evals/s,
+true error, region store size).  Development/measurement helper; the contract
+bench is bench.py (configs[1]).
+
+  python tools/baseline_configs.py [--big-cap LOG2]  > gpurun_out/baseline_configs.json
+
+configs[0] f4 5D 1e-3, configs[2] f2 8D 1e-9, configs[3] f5/f6 8D 1e-8 at the
+reference default cap 2^22 (their finals are in tests/golden/finals*.json), and
+configs[4] f4 10D 1e-7 with the region store sized toward HBM (default cap
+2^28 regions = 93 GB at 10D: 2 x 2 x 8n B of double-buffered geometry + 27 B).
+"""
+import argparse
+import importlib
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2104_06494_b200 as pg  # noqa: E402
+
+suite = importlib.import_module("paper_2104_06494_b200.suite")
+
+
+def run(name, fid, n, tau, cap):
+    cfg = pg.Config(tau_rel=tau, rel_filtering_enabled=fid != 1, max_regions=cap, profile=True)
+    pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n),
+                 pg.Config(tau_rel=1e-3, rel_filtering_enabled=fid != 1, max_regions=cap, it_max=2))  # warm
+    t0 = time.perf_counter()
+    r = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n), cfg)
+    wall = time.perf_counter() - t0
+    exact = suite.reference_value(f"f{fid}", n, corrected=True)
+    return {"config": name, "f": f"f{fid}", "n": n, "tau": tau, "max_regions": cap,
+            "region_store_gb": cap * (32 * n + 27) / 1e9,
+            "status": str(r.status), "iterations": r.iterations, "estimate": r.estimate,
+            "errorest": r.errorest, "true_rel_err": abs(r.estimate - exact) / abs(exact),
+            "regions_generated": r.regions_generated, "peak_regions": r.peak_regions,
+            "region_evals": r.region_evals, "time_to_result_s": r.device_ms / 1e3,
+            "wall_s": wall, "region_evals_per_s": r.region_evals / (r.device_ms / 1e3),
+            "kernel_ms": {k: round(v, 2) for k, v in r.kernel_ms.items()}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big-cap", type=int, default=28)
+    ap.add_argument("--skip-big", action="store_true")
+    a = ap.parse_args()
+    rows = [run("configs[0]", 4, 5, 1e-3, 1 << 22), run("configs[2]", 2, 8, 1e-9, 1 << 22),
+            run("configs[3]", 5, 8, 1e-8, 1 << 22), run("configs[3]", 6, 8, 1e-8, 1 << 22)]
+    if not a.skip_big:
+        rows.append(run("configs[4]", 4, 10, 1e-7, 1 << a.big_cap))
+    print(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()
