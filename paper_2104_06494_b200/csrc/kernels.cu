@@ -204,8 +204,8 @@ inline size_t tree_smem_bytes(int64_t nblk, int groups) {
 // a code (flag ? #{sorted thresholds the error reaches} : 0, see ProbeSet),
 // stored as the 16-bit mask (1 << code) - 1 over sorted positions, and node
 // j's candidates are exactly the regions with bit pos[j] set.  Each step is
-// then LOP3 + 2 FSEL + DADD + IADD (+ 3/8 LDS.128); the err lanes' counters
-// are the candidate counts.
+// then LOP3 + 2 FSEL + DADD (+ 3/8 LDS.128); candidate counts come from a
+// per-block code histogram the producers build with warp-aggregated atomics.
 //
 // Streaming: warps 1..3 stage chunk c+1 (est, err, code; 17 B/region) into a
 // 2-deep shared-memory ring while warp 0 folds chunk c, so a CTA needs only
@@ -217,6 +217,7 @@ struct ProbeStage {
   double est[2][kProbeChunk];
   uint16_t mask[2][kProbeChunk];
   double s[16];
+  unsigned hist[17];  // regions per code (candidate counts = suffix sums)
 };
 
 // ss: the 16 sorted thresholds in shared memory (lane-divergent indices would
@@ -258,6 +259,10 @@ __device__ __forceinline__ void probe_stage_chunk(ProbeStage& S, const ProbeSet&
   for (int u = 0; u < PER; ++u) {
     const int i = t0 + u * nt;
     const uint8_t code = probe_code(S.s, ts.nan_cnt, f[u], e[u]);
+    // one shared atomic per distinct code in the warp (padding regions past
+    // the block end have code 0, which no count reads)
+    const unsigned peers = __match_any_sync(0xffffffffu, static_cast<unsigned>(code));
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&S.hist[code], __popc(peers));
     S.err[buf][i] = e[u];
     S.est[buf][i] = v[u];
     S.mask[buf][i] = static_cast<uint16_t>((1u << code) - 1u);
@@ -267,11 +272,8 @@ __device__ __forceinline__ void probe_stage_chunk(ProbeStage& S, const ProbeSet&
 // s += v unless (word & bit) (the skip of reduce.cpp:59-60; adding +0.0
 // instead is identical: s starts at +0.0 and never becomes -0.0 under RN).
 // The select happens on the loaded value, off the DADD dependency chain.
-__device__ __forceinline__ void add_unless(double& s, double v, uint32_t word, uint32_t bit,
-                                           int& c) {
-  const bool cand = (word & bit) != 0;
-  c += cand;
-  s = P_ADD(s, cand ? 0.0 : v);
+__device__ __forceinline__ void add_unless(double& s, double v, uint32_t word, uint32_t bit) {
+  s = P_ADD(s, (word & bit) ? 0.0 : v);
 }
 
 __global__ void __launch_bounds__(kProbeThreads)
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(kProbeThreads)
   const int nch = (n + kProbeChunk - 1) / kProbeChunk;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid < 16) S.s[tid] = ts.s[tid];
+  if (tid < 17) S.hist[tid] = 0;
   __syncthreads();
   probe_stage_chunk<kProbeChunk / kProbeThreads>(S, ts, est, err, flag, lo, n, 0, tid,
                                                  kProbeThreads);
@@ -293,7 +296,6 @@ __global__ void __launch_bounds__(kProbeThreads)
   const int pos = ts.pos[node];
   const int q = lane >> 4;  // 0: err chain, 1: est chain
   double fin = 0.0;
-  int cc = 0;  // candidates of node `node` in this block
   for (int c = 0; c < nch; ++c) {
     if (w > 0) {
       if (c + 1 < nch)
@@ -313,24 +315,28 @@ __global__ void __launch_bounds__(kProbeThreads)
           const double2 v1 = *reinterpret_cast<const double2*>(x + i + 2);
           const double2 v2 = *reinterpret_cast<const double2*>(x + i + 4);
           const double2 v3 = *reinterpret_cast<const double2*>(x + i + 6);
-          add_unless(fin, v0.x, m8.x, blo, cc);
-          add_unless(fin, v0.y, m8.x, bhi, cc);
-          add_unless(fin, v1.x, m8.y, blo, cc);
-          add_unless(fin, v1.y, m8.y, bhi, cc);
-          add_unless(fin, v2.x, m8.z, blo, cc);
-          add_unless(fin, v2.y, m8.z, bhi, cc);
-          add_unless(fin, v3.x, m8.w, blo, cc);
-          add_unless(fin, v3.y, m8.w, bhi, cc);
+          add_unless(fin, v0.x, m8.x, blo);
+          add_unless(fin, v0.y, m8.x, bhi);
+          add_unless(fin, v1.x, m8.y, blo);
+          add_unless(fin, v1.y, m8.y, bhi);
+          add_unless(fin, v2.x, m8.z, blo);
+          add_unless(fin, v2.y, m8.z, bhi);
+          add_unless(fin, v3.x, m8.w, blo);
+          add_unless(fin, v3.y, m8.w, bhi);
         }
       } else {
-        for (int i = 0; i < cntc; ++i) add_unless(fin, x[i], mk[i], 1u << pos, cc);
+        for (int i = 0; i < cntc; ++i) add_unless(fin, x[i], mk[i], 1u << pos);
       }
     }
     __syncthreads();
   }
   if (w == 0 && (lane & 15) < ts.T) {
     part[(q * kMaxProbes + node) * nblk + b] = fin;
-    if (q == 0) cnt[node * nblk + b] = cc;
+    if (q == 0) {
+      int64_t c = 0;  // candidates of node j: regions whose code exceeds pos[j]
+      for (int k = pos + 1; k <= 16; ++k) c += S.hist[k];
+      cnt[node * nblk + b] = c;
+    }
   }
 }
 
