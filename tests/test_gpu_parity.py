@@ -317,6 +317,22 @@ def test_integrate_matches_reference_finals_8d(pg, gpu):
         assert len(res.threshold_events) == want["n_events"], name
 
 
+def test_integrate_matches_reference_finals_deep(pg, gpu):
+    """Every BASELINE config at full size against the reference's own final
+    results (tests/golden/finals_deep.json, made by make_deep_finals.py with
+    the unmodified reference: tens of CPU-minutes): the whole 8D suite
+    f1..f6 x tau 1e-3..1e-6 (bench.py's workload), f2 8D 1e-9, f5 / f6 8D 1e-8.
+    Bit-exact estimates and errors, identical status, iterations, region and
+    evaluation counts and threshold-event counts."""
+    cases = load_golden("finals_deep.json")
+    assert len(cases) >= 6
+    for name, want in cases.items():
+        cfg = pg.Config(tau_rel=want["tau"], rel_filtering_enabled=want["fid"] != 1)
+        res = pg.integrate(pg.Integrand(want["fid"]), pg.Bounds.unit_cube(want["n"]), cfg)
+        assert_same_result(res, want)
+        assert len(res.threshold_events) == min(want["n_events"], 256), name
+
+
 MORE_CASES = [
     ("mapped_xy", 101, 2, 1e-6, True, {}, [1, 1], ([0, 1], [2, 3])),
     ("mapped_f4", 4, 3, 1e-4, True, {}, None, ([-1, 0, 0.25], [1, 2, 0.75])),
