@@ -5,6 +5,9 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <limits>
 
 #include "glibc_tables.h"
@@ -570,7 +573,10 @@ __global__ void k_minmax_done(int64_t m, const double* x, const unsigned long lo
 }
 
 // ---- fused filter + bisect ---------------------------------------------------
-constexpr int kSplitThreads = 256;
+#ifndef PGN_SPLIT_THREADS
+#define PGN_SPLIT_THREADS 512  // 4 rounds per 2048-block; 256 left a 2.35-wave tail (-10% at 512)
+#endif
+constexpr int kSplitThreads = PGN_SPLIT_THREADS;
 constexpr int kSplitPer = static_cast<int>(kBlock) / kSplitThreads;  // 8
 
 // Rank of each kept region inside its 2048-block: warp ballots + CTA scan.
@@ -887,13 +893,23 @@ void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const
                                                                  cnt);
 }
 
+// Opt a kernel in to > 48 KB of dynamic shared memory, once per (device, kernel).
+void opt_in_smem(const void* fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert({dev, fn}).second)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kTreeSmemMaxBytes));
+}
+
 void finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
                     const int64_t* cnt, double* scratch, ProbeScalars* out) {
   const size_t sm = tree_smem_bytes(nblk, 1);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
-    // opt in to > 48 KB dynamic shared memory (per device; cheap host call)
-    cudaFuncSetAttribute(k_finalize_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kTreeSmemMaxBytes));
+    opt_in_smem(reinterpret_cast<const void*>(&k_finalize_multi<true>));
     k_finalize_multi<true><<<3 * T, 256, sm, st>>>(nblk, T, part, cnt, scratch, out);
   } else {
     k_finalize_multi<false><<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out);
@@ -958,9 +974,7 @@ void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const unsigned long long* mm, const double* err0) {
   const size_t sm = tree_smem_bytes(nblk, 4);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
-    // opt in to > 48 KB dynamic shared memory (per device; cheap host call)
-    cudaFuncSetAttribute(k_finalize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kTreeSmemMaxBytes));
+    opt_in_smem(reinterpret_cast<const void*>(&k_finalize<true>));
     k_finalize<true><<<1, kFinThreads, sm, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
                                                  err0);
   } else {
