@@ -15,6 +15,7 @@
 // per-iteration trace field with the reference library).
 #include "driver.hpp"
 
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -75,6 +76,11 @@ void Workspace::ensure(int n_, int64_t cap_) {
     PGN_CK(cudaMallocHost(&h_mm, 4 * sizeof(double)));
     d_probe.alloc(1);
     PGN_CK(cudaMallocHost(&h_probe, sizeof(ProbeScalars)));
+    PGN_CK(cudaHostAlloc(&h_zc, sizeof(FoldScalars), cudaHostAllocMapped));
+    PGN_CK(cudaHostAlloc(&h_ready, 64, cudaHostAllocMapped));
+    *reinterpret_cast<volatile unsigned*>(h_ready) = 0;
+    PGN_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_zc), h_zc, 0));
+    PGN_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ready), h_ready, 0));
   }
   n = nn;
   cap = nc;
@@ -95,6 +101,8 @@ Workspace::~Workspace() {
   if (h_sc) cudaFreeHost(h_sc);
   if (h_mm) cudaFreeHost(h_mm);
   if (h_probe) cudaFreeHost(h_probe);
+  if (h_zc) cudaFreeHost(h_zc);
+  if (h_ready) cudaFreeHost(h_ready);
   if (h_kb) cudaFreeHost(h_kb);
   if (st) cudaStreamDestroy(st);
 }
@@ -254,6 +262,26 @@ int initial_subdivisions(int n, int64_t init_target) {  // geometry.cpp:67-81
     ++d;
   }
   return d;
+}
+
+// ---------------------------------------------------------------------------
+// Spin until the device publishes `seq` at *flag (k_finalize's zero-copy
+// hand-off), checking the stream for errors now and then so a failed launch
+// cannot hang the host.
+void wait_host_flag(const unsigned* flag, unsigned seq, cudaStream_t st) {
+  const volatile unsigned* f = flag;
+  for (uint64_t i = 0;; ++i) {
+    if (*f == seq) break;
+    if ((i & 4095) == 4095) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e == cudaSuccess) {
+        if (*f == seq) break;
+        throw CudaError("zero-copy hand-off: stream idle but the scalars were not published");
+      }
+      if (e != cudaErrorNotReady) cuda_check(e, "k_finalize (zero-copy hand-off)");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 // ---------------------------------------------------------------------------
@@ -617,9 +645,11 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     }
     const size_t k2 = kt.mark();
     const int64_t* offsets = ws.off_eval.p;  // kept offsets, indexed by (global) block
+    const bool zero_copy = !sh;
     if (!sh) {
       launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
-                      ws.d_sc.p, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p);
+                      ws.d_zc, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p, ws.d_ready,
+                      ++ws.seq);
       out->kernel_launches[PAGANI_K_FINALIZE]++;
     } else {  // allgather the block records; every rank runs the same global trees
       launch_pack_blocks(st, nblk, sh->nblk_max, ws.part_eval.p, ws.cnt_eval.p, ws.mm_blk.p,
@@ -638,8 +668,13 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     const size_t k3 = kt.mark();
     kt.span(PAGANI_K_FOLD, k1, k2);
     kt.span(PAGANI_K_FINALIZE, k2, k3);
-    PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
-    PGN_CK(cudaStreamSynchronize(st));
+    if (zero_copy) {
+      wait_host_flag(ws.h_ready, ws.seq, st);
+      ws.h_sc[0] = *ws.h_zc;
+    } else {
+      PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
+      PGN_CK(cudaStreamSynchronize(st));
+    }
     out->d2h_bytes += sizeof(FoldScalars);
     if (sh)
       for (int r = 0; r <= R; ++r) kb[r] = ws.h_kb[r];

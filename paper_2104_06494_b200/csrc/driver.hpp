@@ -86,6 +86,12 @@ struct Workspace {
   DevBuf<unsigned long long> mm_keys;
   DevBuf<double> mm_out, d_lower, d_step, d_tmp;
   FoldScalars* h_sc = nullptr;  // pinned [2]
+  // zero-copy per-iteration scalars (mapped pinned memory, see k_finalize)
+  FoldScalars* h_zc = nullptr;
+  FoldScalars* d_zc = nullptr;  // device alias of h_zc
+  unsigned* h_ready = nullptr;
+  unsigned* d_ready = nullptr;
+  unsigned seq = 0;
   double* h_mm = nullptr;       // pinned [4]
   std::vector<cudaEvent_t> ev;
   void ensure(int n, int64_t cap);

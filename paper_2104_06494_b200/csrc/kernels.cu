@@ -437,11 +437,26 @@ __global__ void k_fold_one(int64_t m, int64_t nblk, const double* __restrict__ x
 constexpr int kFinThreads = 1024;
 
 
+// Zero-copy hand-off of the per-iteration scalars: `out` lives in mapped
+// pinned host memory; the threads that wrote a field of it (tid 0: min/max,
+// tid % 256 == 0: the tree sums, the last thread: the count) fence their
+// writes at system scope, then one thread publishes the sequence number the
+// host is spinning on.
+__device__ __forceinline__ void signal_host(unsigned* ready, unsigned seq) {
+  if (!ready) return;
+  if ((threadIdx.x & 255) == 0 || threadIdx.x == blockDim.x - 1) __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(ready) = seq;
+  }
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(kFinThreads)
     k_finalize(int64_t nblk, int nq, const double* part, const int64_t* cnt, int64_t* offsets,
                double* scratch, FoldScalars* out, const unsigned long long* mm,
-               const double* err0) {
+               const double* err0, unsigned* ready, unsigned seq) {
   extern __shared__ double s_tree[];
   __shared__ int64_t s_sum[kFinThreads];
   __shared__ unsigned long long s_k[2][kFinThreads / 32];
@@ -507,6 +522,7 @@ __global__ void __launch_bounds__(kFinThreads)
   }
   if (!cnt) {
     if (tid == 0) out->count = 0;
+    signal_host(ready, seq);
     return;
   }
   // exclusive scan of per-block counts (exact integers)
@@ -529,6 +545,7 @@ __global__ void __launch_bounds__(kFinThreads)
       run += cnt[i];
     }
   if (tid == kFinThreads - 1) out->count = s_sum[tid];
+  signal_host(ready, seq);
 }
 
 // ---- min / max ---------------------------------------------------------------
@@ -971,15 +988,16 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
-                     const unsigned long long* mm, const double* err0) {
+                     const unsigned long long* mm, const double* err0, unsigned* ready,
+                     unsigned seq) {
   const size_t sm = tree_smem_bytes(nblk, 4);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
     opt_in_smem(reinterpret_cast<const void*>(&k_finalize<true>));
     k_finalize<true><<<1, kFinThreads, sm, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
-                                                 err0);
+                                                 err0, ready, seq);
   } else {
     k_finalize<false><<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
-                                                 err0);
+                                                  err0, ready, seq);
   }
 }
 

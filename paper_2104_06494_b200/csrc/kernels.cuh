@@ -83,9 +83,12 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 
 // Pairwise trees over nq partial arrays (stride nblk) + exclusive scan of cnt
 // (+ min/max of the errors from per-block keys mm, if given; err0 = &err[0]).
+// With `ready`, `out` is mapped pinned host memory and the kernel publishes
+// `seq` at *ready once every field is visible to the host (zero-copy hand-off).
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
-                     const unsigned long long* mm = nullptr, const double* err0 = nullptr);
+                     const unsigned long long* mm = nullptr, const double* err0 = nullptr,
+                     unsigned* ready = nullptr, unsigned seq = 0);
 
 // T speculative probes in one pass + their trees; part [2][kMaxProbes][nblk],
 // cnt [kMaxProbes][nblk], scratch 2*3*kMaxProbes*nblk doubles.
