@@ -214,6 +214,10 @@ inline size_t tree_smem_bytes(int64_t nblk, int groups) {
 // 2-deep shared-memory ring while warp 0 folds chunk c, so a CTA needs only
 // 13.9 KB and every block of a 2^22-region batch is resident at once.
 constexpr int kProbeThreads = 128;
+#ifndef PGN_PROBE_UNROLL
+#define PGN_PROBE_UNROLL 2
+#endif
+constexpr int kProbeUnroll = PGN_PROBE_UNROLL;
 constexpr int kProbeChunk = 384;  // = 4 x 96 producer threads = 3 x 128
 struct ProbeStage {
   double err[2][kProbeChunk];
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(kProbeThreads)
       const int cntc = n - c * kProbeChunk < kProbeChunk ? n - c * kProbeChunk : kProbeChunk;
       if (cntc == kProbeChunk) {
         const uint32_t blo = 1u << pos, bhi = blo << 16;
-#pragma unroll 2
+#pragma unroll kProbeUnroll
         for (int i = 0; i < kProbeChunk; i += 8) {
           const uint4 m8 = *reinterpret_cast<const uint4*>(mk + i);
           const double2 v0 = *reinterpret_cast<const double2*>(x + i);
