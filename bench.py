@@ -227,6 +227,17 @@ def run_ours(args, rank, world, local_rank):
                          "true_rel_err_le_tau": bool(true_rel is not None and true_rel <= tau),
                          "time_to_result_s": r.device_ms / 1e3})
     achieved = flops / (eval_ms / 1e3) / 1e12 if eval_ms > 0 else 0.0
+    # per integrand: the algorithmic count is the reference's arithmetic, so an
+    # integrand whose per-point work the separable evaluator shares (f2: the n
+    # divisions per point become 9n per region) can exceed the peak; ncu's
+    # FP64-pipe utilisation is the executed-work view.
+    per_f = {}
+    for fid in sorted({f for f, _ in cases}):
+        ms = sum(r.kernel_ms["evaluate"] for st in steps for f, _, r in st if f == fid)
+        fl = sum(r.region_evals * roofline.region_flops(f, DIM) for st in steps
+                 for f, _, r in st if f == fid)
+        if ms > 0:
+            per_f[f"f{fid}"] = round(fl / (ms / 1e3) / 1e12, 2)
     # HBM rooflines of the memory-side kernels: algorithmic bytes (DESIGN.md 4,
     # counted by the driver per launch) / their CUDA-event time.
     hbm_peak, hbm_src = measured_hbm_peak()
@@ -268,6 +279,7 @@ def run_ours(args, rank, world, local_rank):
                      "peak_source": f"measured live: DFMA microbenchmark (pagani_fp64_peak) at "
                                     f"{peak_mhz:.0f} MHz; MEASURED_PEAKS.json has no FP64 entry",
                      "flops_model": "SURVEY.md 8(d) F(f,n), paper_2104_06494_b200/roofline.py",
+                     "tflops_per_integrand": per_f,
                      "eval_ms": eval_ms / args.steps, "eval_launches": eval_launches // args.steps,
                      "eval_share_of_step": eval_ms / dev_ms if dev_ms else None,
                      "kernel_ms_per_step": {k: round(sum(r.kernel_ms[k] for st in steps
