@@ -431,3 +431,50 @@ def test_large_batch_properties(pg, gpu):
         assert nxt["v_f"] == prev["v_f"] + prev["fin_v"]
         assert nxt["e_f"] == prev["e_f"] + prev["fin_e"]
     assert max(ms) <= 1 << 22
+
+
+def test_batch_functions_on_empty_and_tiny_inputs(pg, gpu, ref):
+    """Empty and one/odd-element inputs through every batch entry point (the
+    reference's functions accept them: reduce.cpp:13-82, classify.cpp:11-129,
+    geometry.cpp:114-143, rule.cpp:351-430)."""
+    for m in (0, 1, 2, 3, 2047, 2049):
+        rng = np.random.default_rng(m)
+        n = 3
+        lows = rng.uniform(0.0, 0.5, size=(m, n))
+        lens = rng.uniform(0.01, 0.5, size=(m, n))
+        est, raw, axes, cnt = pg.evaluate_batch(pg.Integrand(4), lows, lens)
+        e2, r2, a2, c2 = ref.evaluate_batch(4, lows, lens)
+        assert len(est) == m and cnt == c2
+        assert np.array_equal(bits(est), bits(e2)) and np.array_equal(bits(raw), bits(r2))
+        assert np.array_equal(axes, a2)
+        x = rng.uniform(-1.0, 1.0, size=m)
+        assert np.array_equal(bits([pg.block_sum(x)]), bits([ref.block_sum(x)]))
+        fl = (rng.uniform(size=m) < 0.5).astype(np.uint8)
+        for which in (0, 1):
+            assert np.array_equal(bits([pg.block_sum_where(x, fl, which)]),
+                                  bits([ref.block_sum_where(x, fl, which)]))
+        err = np.abs(raw)
+        assert np.array_equal(pg.rel_err_classify(est, err, 1e-3), ref.rel_err_classify(est, err, 1e-3))
+        if m % 2 == 0:  # siblings come in pairs
+            pest = rng.uniform(0.0, 1.0, size=m)
+            perr = rng.uniform(0.0, 1.0, size=m)
+            assert np.array_equal(bits(pg.two_level_refine(est, raw, pest, perr)),
+                                  bits(ref.two_level_refine(est, raw, pest, perr)))
+        b = pg.RegionBatch(lows, lens, est, err, axes)
+        fr = pg.filter(b, fl)
+        want = ref.filter(lows, lens, est, err, axes, np.zeros(m), np.zeros(m), fl)
+        assert fr.kept.count == want["kept"]
+        assert np.array_equal(bits(fr.kept.lows), bits(want["lows"]))
+        assert np.array_equal(bits([fr.finished_estimate, fr.finished_error]),
+                              bits([want["finished_estimate"], want["finished_error"]]))
+        kids = pg.bisect(b, 1 << 22)
+        cl, cn, cp, cq = ref.bisect(lows, lens, est, err, axes)
+        assert np.array_equal(bits(kids.lows), bits(cl)) and np.array_equal(bits(kids.lengths), bits(cn))
+        if m:
+            act = np.ones(m, dtype=np.uint8)
+            got = pg.threshold_classify(act, err, float(est.sum()), float(err.sum()),
+                                        float(err.sum()), m, 1e-3)
+            exp = ref.threshold_classify(act, err, float(est.sum()), float(err.sum()),
+                                         float(err.sum()), m, 1e-3)
+            assert got.success == exp["success"] and got.attempts == exp["attempts"]
+            assert np.array_equal(got.flags, exp["flags"])
