@@ -145,28 +145,6 @@ __global__ void __launch_bounds__(kFoldThreads)
   part[(q + 2) * nblk + b] = fin;
 }
 
-// Threshold probe: q0 = sum err[cand==0], q1 = sum est[cand==0],
-// cnt = #cand==1 with cand = flag & !(err < t)  (classify.cpp:63-70, 104-105).
-__global__ void __launch_bounds__(kFoldThreads)
-    k_probe(int64_t m, int64_t nblk, double t, const double* __restrict__ est,
-            const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
-            int64_t* cnt) {
-  __shared__ FoldSmem S;
-  const int64_t b = blockIdx.x;
-  const int64_t lo = b * kBlock;
-  const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
-  const int64_t active = stage_block(S, est, err, flag, lo, n, true, t, true);
-  if ((threadIdx.x & 31) != 0 || threadIdx.x >= 64) {
-    if (threadIdx.x == 64) cnt[b] = active;
-    return;
-  }
-  const double* x = threadIdx.x == 0 ? S.err : S.est;
-  double fin = 0.0;
-#pragma unroll 8
-  for (int i = 0; i < n; ++i) fin = P_ADD(fin, S.flag[i] ? 0.0 : x[i]);
-  part[(threadIdx.x == 0 ? 0 : 1) * nblk + b] = fin;
-}
-
 // Pairwise tree (reduce.cpp:13-27: p[i] = p[2i] + p[2i+1], odd tail carried)
 // of src[0..n) by a group of gn threads (local id lt).  The first level reads
 // the global partials, every later level runs in shared memory (`sm`, room for
@@ -906,13 +884,6 @@ void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const doubl
                                                                      part, cnt);
 }
 
-void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const double* err,
-                  const uint8_t* flag, double* part, int64_t* cnt) {
-  const int64_t nblk = nblocks_of(m);
-  if (nblk == 0) return;
-  k_probe<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, t, est, err, flag, part,
-                                                                 cnt);
-}
 
 // Opt a kernel in to > 48 KB of dynamic shared memory, once per (device, kernel).
 void opt_in_smem(const void* fn) {

@@ -69,11 +69,7 @@ void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap,
 void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
                       const uint8_t* flag, double* part, int64_t* cnt);
 
-// Threshold probe (classify.cpp:63-70): cand = flag & !(err < t);
-// q0 = sum err[cand==0], q1 = sum est[cand==0], count(cand==1) -> cnt.
-// Candidates are never materialised: k_split re-derives them from t.
-void launch_probe(cudaStream_t st, int64_t m, double t, const double* est, const double* err,
-                  const uint8_t* flag, double* part, int64_t* cnt);
+// Candidate flags of an accepted threshold (classify.cpp:63-66), batch API.
 void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,
                        const double* err, uint8_t* out);
 
