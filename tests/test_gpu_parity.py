@@ -333,6 +333,18 @@ def test_integrate_matches_reference_finals_deep(pg, gpu):
         assert len(res.threshold_events) == min(want["n_events"], 256), name
 
 
+def test_integrate_matches_reference_finals_bigcap(pg, gpu):
+    """A 2^24-region cap (8192 fold blocks): the global-memory tree path of
+    the finalize kernels and 8192-block probe passes, against the reference's
+    finals at the same cap (tests/golden/finals_bigcap.json)."""
+    for name, want in load_golden("finals_bigcap.json").items():
+        cfg = pg.Config(tau_rel=want["tau"], rel_filtering_enabled=want["fid"] != 1,
+                        max_regions=want["max_regions"])
+        res = pg.integrate(pg.Integrand(want["fid"]), pg.Bounds.unit_cube(want["n"]), cfg)
+        assert_same_result(res, want)
+        assert len(res.threshold_events) == min(want["n_events"], 256), name
+
+
 MORE_CASES = [
     ("mapped_xy", 101, 2, 1e-6, True, {}, [1, 1], ([0, 1], [2, 3])),
     ("mapped_f4", 4, 3, 1e-4, True, {}, None, ([-1, 0, 0.25], [1, 2, 0.75])),
