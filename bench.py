@@ -306,7 +306,10 @@ def ref_sample(ref, make_config):
     evals = 0
     t0 = time.perf_counter()
     for fid in FIDS:
-        cfg = make_config(tau_rel=1e-3, it_max=CPU_SAMPLE_IT_MAX, rel_filtering_enabled=(fid != 1))
+        # threads = every host core explicitly (Config::threads -> omp_set_num_threads,
+        # driver.cpp): torchrun exports OMP_NUM_THREADS=1 to its workers
+        cfg = make_config(tau_rel=1e-3, it_max=CPU_SAMPLE_IT_MAX, rel_filtering_enabled=(fid != 1),
+                          threads=os.cpu_count() or 1)
         r = ref.integrate(fid, DIM, cfg)
         evals += r.eval_count // ((1 << DIM) + 2 * DIM * (DIM - 1) + 4 * DIM + 1)
     return evals, time.perf_counter() - t0
