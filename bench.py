@@ -41,9 +41,16 @@ UNIT = "region-evals/s"
 DIM = 8
 TAUS = (1e-3, 1e-4, 1e-5, 1e-6)
 FIDS = (1, 2, 3, 4, 5, 6)
-# Bounded CPU sample of the same workload: f1..f6 8D tau=1e-3, first 9 iterations.
-CPU_SAMPLE_IT_MAX = 9
-CPU_SAMPLE_DESC = "f1..f6 8D tau=1e-3 with it_max=9 (first 9 PAGANI iterations of each)"
+# Bounded CPU sample of the same workload: a faithful subset of the suite --
+# two of its 24 integrate() calls, run to their end exactly as in the suite
+# (same config, same outcome), ~5-10 s of reference CPU time per step.  The GPU
+# arm runs the same two calls inside its timed steps and reports its rate on
+# them ("same_sample"), so the GPU/CPU ratio on identical work is derivable.
+CPU_SAMPLE = ((3, 1e-3), (3, 1e-4))
+CPU_SAMPLE_DESC = ("complete integrate() calls f3@1e-3 + f3@1e-4 (8D, suite config: "
+                   "2 of the suite's 24 cases, run to their end)")
+# 1-thread protocol run: the first of the two calls
+CPU_SAMPLE_1T = ((3, 1e-3),)
 
 
 def dist_env():
@@ -121,6 +128,56 @@ def measured_hbm_peak():
         return 6650.0, "of fallback: 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
+def bench_config(args):
+    """The workload's config, identical in both arms (the reference arm times a
+    bounded sample of this same workload; its cpu_baseline.sample says which)."""
+    return {"workload": "genz_8d_suite: f1..f6 x tau in {1e-3,1e-4,1e-5,1e-6}, n=8, "
+                        "tau_abs=1e-20, it_max=100, rel filter off for f1",
+            "max_regions": args.max_regions, "mode": args.mode,
+            "l2": "working set > L2: each run streams a region store of up to 1.1 GB"}
+
+
+try:  # before any OpenMP runtime binds this thread (OMP_PROC_BIND shrinks the mask)
+    _USABLE_CPUS = len(os.sched_getaffinity(0))
+except Exception:  # noqa: BLE001
+    _USABLE_CPUS = os.cpu_count()
+
+
+def host_cpu():
+    """CPU model and core counts from lscpu."""
+    info = {"model": None, "sockets": 1, "cores_per_socket": None, "threads_per_core": 1,
+            "logical": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        info["sockets"] = int(kv.get("Socket(s)", "1") or 1)
+        info["cores_per_socket"] = int(kv.get("Core(s) per socket", "0") or 0) or None
+        info["threads_per_core"] = int(kv.get("Thread(s) per core", "1") or 1)
+    except Exception:  # noqa: BLE001
+        pass
+    if info["cores_per_socket"]:
+        info["physical"] = info["sockets"] * info["cores_per_socket"]
+    else:
+        info["physical"] = max(1, (os.cpu_count() or 1) // max(1, info["threads_per_core"]))
+    info["usable"] = _USABLE_CPUS
+    return info
+
+
+def load_reference():
+    """The unmodified reference (oracle/_ref).  OpenMP placement must be in the
+    environment before libgomp initialises, i.e. before the library loads."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from ref_ctypes import Ref, make_config
+    return Ref(), make_config
+
+
 # --------------------------------------------------------------- ours -------
 def run_ours(args, rank, world, local_rank):
     import paper_2104_06494_b200 as pg
@@ -170,12 +227,18 @@ def run_ours(args, rank, world, local_rank):
     mode = args.mode
     cases = workload(args.cases)
 
-    def one_step(profile):
+    call_wall = {}  # (fid, tau) -> host wall seconds of each timed call
+
+    def one_step(profile, timed=False):
         rs = []
         for fid, tau in cases:
             cfg = pg.Config(tau_rel=tau, rel_filtering_enabled=(fid != 1), max_regions=args.max_regions,
                             mode=mode, device=device, profile=profile, comm=comm)
-            rs.append((fid, tau, pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(DIM), cfg)))
+            t0 = time.perf_counter()
+            r = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(DIM), cfg)
+            if timed:
+                call_wall[(fid, tau)] = call_wall.get((fid, tau), 0.0) + time.perf_counter() - t0
+            rs.append((fid, tau, r))
         return rs
 
     for _ in range(args.warmup):
@@ -190,7 +253,7 @@ def run_ours(args, rank, world, local_rank):
     t_wall0 = time.perf_counter()
     steps = []
     for _ in range(args.steps):
-        steps.append(one_step(True))
+        steps.append(one_step(True, timed=True))
     barrier_sync()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
@@ -258,20 +321,32 @@ def run_ours(args, rank, world, local_rank):
             traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # the GPU's rate on exactly the reference arm's sample (same calls, taken
+    # from the timed steps above)
+    same = None
+    samp = [c for c in CPU_SAMPLE if c in set(cases)]
+    if samp:
+        ev = sum(r.region_evals for st in steps for f, t, r in st if (f, t) in samp)
+        ms = sum(r.device_ms for st in steps for f, t, r in st if (f, t) in samp)
+        wall = sum(call_wall.get(c, 0.0) for c in samp)
+        same = {"sample": CPU_SAMPLE_DESC, "value": ev / (ms / 1e3) if ms else None,
+                "e2e_value": ev / wall if wall else None, "unit": UNIT,
+                "region_evals_per_step": ev // args.steps,
+                "ms_per_step": ms / args.steps}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
+        if same and cpu.get("value"):
+            same["vs_cpu_baseline"] = same["value"] / cpu["value"]
+            same["e2e_vs_cpu_baseline"] = (same["e2e_value"] or 0.0) / cpu["value"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_s_max * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "strong" if comm is not None or world == 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's fixed-parameter Genz integrands (deterministic, no dataset)",
-        "config": {"workload": "genz_8d_suite: f1..f6 x tau in {1e-3,1e-4,1e-5,1e-6}, n=8, "
-                               "tau_abs=1e-20, it_max=100, rel filter off for f1",
-                   "max_regions": args.max_regions, "mode": mode,
-                   "l2": "working set > L2: each run streams a region store of up to 1.1 GB",
-                   "parallelism": parallelism},
+        "config": bench_config(args),
+        "parallelism": parallelism,
         "roofline": {"bound": "fp64", "kernel": "k_evaluate_sep", "achieved": achieved,
                      "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": achieved / peak_tflops if peak_tflops else None,
@@ -291,6 +366,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "clocks": clk,
+        "same_sample": same,
         "time_to_tolerance_s": {f"{c['f']}@{c['tau']:g}": round(c["time_to_result_s"], 6)
                                 for c in per_case},
         "outcomes": per_case,
@@ -301,45 +377,67 @@ def run_ours(args, rank, world, local_rank):
 
 
 # --------------------------------------------------------------- reference --
-def ref_sample(ref, make_config):
-    """One bounded sample of the workload on the reference library."""
+def ref_sample(ref, make_config, threads, cases=CPU_SAMPLE):
+    """One bounded sample of the workload on the reference library: complete
+    integrate() calls of suite cases (suite config), timed with a steady clock
+    around each call as the reference CLI does (bfcub_cli.cpp:81-83)."""
     evals = 0
-    t0 = time.perf_counter()
-    for fid in FIDS:
-        # threads = every host core explicitly (Config::threads -> omp_set_num_threads,
-        # driver.cpp): torchrun exports OMP_NUM_THREADS=1 to its workers
-        cfg = make_config(tau_rel=1e-3, it_max=CPU_SAMPLE_IT_MAX, rel_filtering_enabled=(fid != 1),
-                          threads=os.cpu_count() or 1)
+    secs = 0.0
+    for fid, tau in cases:
+        # Config::threads -> omp_set_num_threads (driver.cpp); torchrun exports
+        # OMP_NUM_THREADS=1 to its workers, so it is set explicitly
+        cfg = make_config(tau_rel=tau, rel_filtering_enabled=(fid != 1), threads=threads)
+        t0 = time.perf_counter()
         r = ref.integrate(fid, DIM, cfg)
+        secs += time.perf_counter() - t0
         evals += r.eval_count // ((1 << DIM) + 2 * DIM * (DIM - 1) + 4 * DIM + 1)
-    return evals, time.perf_counter() - t0
+    return evals, secs
+
+
+def cpu_desc(cpu, threads):
+    return (f"{cpu['model']}: {cpu['physical']} physical cores ({cpu['sockets']} socket(s) x "
+            f"{cpu['cores_per_socket']} cores x {cpu['threads_per_core']} threads/core, "
+            f"{cpu['logical']} logical, {cpu['usable']} usable); OpenMP threads = {threads}, "
+            f"OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')} OMP_PLACES={os.environ.get('OMP_PLACES')}")
+
+
+def one_thread_rate(ref, make_config):
+    e, s = ref_sample(ref, make_config, 1, CPU_SAMPLE_1T)
+    return {"value": e / s, "unit": UNIT, "threads": 1,
+            "sample": "complete integrate() call f3@1e-3 (8D, suite config)",
+            "region_evals": e, "seconds": round(s, 3)}
 
 
 def cpu_baseline():
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from ref_ctypes import Ref, make_config
-    ref = Ref()
-    evals, secs = ref_sample(ref, make_config)
-    return {"value": evals / secs, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-            "sample": CPU_SAMPLE_DESC + f"; {evals} region-evals in {secs:.1f} s, OpenMP "
-                      f"threads = all {os.cpu_count()} host cores"}
+    """The reference on the box's host cores: the bounded sample with every
+    usable core (median of 3, the runs are < 60 s) and the 1-thread rate."""
+    cpu = host_cpu()
+    threads = cpu["usable"] or cpu["logical"] or 1
+    ref, make_config = load_reference()
+    runs = [ref_sample(ref, make_config, threads) for _ in range(3)]
+    evals, secs = sorted(runs, key=lambda r: r[1])[1]
+    return {"value": evals / secs, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": CPU_SAMPLE_DESC + f"; {evals} region-evals in {secs:.2f} s (median of 3)",
+            "host": cpu_desc(cpu, threads), "cpu_model": cpu["model"],
+            "physical_cores": cpu["physical"], "logical_cpus": cpu["logical"],
+            "one_thread": one_thread_rate(ref, make_config)}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    cpu = host_cpu()
+    threads = cpu["usable"] or cpu["logical"] or 1
     try:
-        from ref_ctypes import Ref, make_config
-        ref = Ref()
+        ref, make_config = load_reference()
     except Exception as e:  # the reference is compiled in-tree; this should not happen
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not loadable: {e}"}))
         return
     for _ in range(args.warmup):
-        ref_sample(ref, make_config)
+        ref_sample(ref, make_config, threads)
     tot_e, tot_s = 0, 0.0
     for _ in range(args.steps):
-        e, s = ref_sample(ref, make_config)
+        e, s = ref_sample(ref, make_config, threads)
         tot_e += e
         tot_s += s
     value = tot_e / tot_s
@@ -348,13 +446,35 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's fixed-parameter Genz integrands (deterministic)",
-        "config": {"workload": "genz_8d_suite (bounded sample per step: " + CPU_SAMPLE_DESC + ")",
-                   "max_regions": 1 << 22, "mode": "reference CPU (bfcub, OpenMP)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(),
-                         "kind": "reference", "sample": CPU_SAMPLE_DESC},
+        "config": bench_config(args),
+        "parallelism": "reference CPU (bfcub, OpenMP), rank 0 only",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": CPU_SAMPLE_DESC, "host": cpu_desc(cpu, threads),
+                         "cpu_model": cpu["model"], "physical_cores": cpu["physical"],
+                         "logical_cpus": cpu["logical"],
+                         "one_thread": one_thread_rate(ref, make_config)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_distributed(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: start the N ranks here,
+    one process per GPU, exactly as the driver's torchrun command does."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and not (args.dist_backend == "gloo" and have >= 1):
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} GPU(s) visible"}),
+              flush=True)
+        sys.exit(2)
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -372,6 +492,12 @@ def main():
                     help="profiling subset, e.g. f4@1e-3 (the default is the whole suite)")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_distributed(args)  # does not return
+    if args.impl == "ours" and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank "
+                                   f"per GPU (torchrun --nproc-per-node {args.gpus})"}), flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

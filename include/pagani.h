@@ -167,6 +167,9 @@ typedef struct pagani_threshold_event {
 #define PAGANI_K_PROBE 4    /* threshold probes */
 #define PAGANI_K_SPLIT 5    /* filter + bisect */
 #define PAGANI_K_INIT 6     /* uniform split */
+#define PAGANI_K_EXCHANGE 7 /* sharded runs: post-bisection region exchange; kernel_bytes =
+                               bytes this rank sent to peers (region geometry + parent est),
+                               kernel_launches = exchanges with a peer transfer */
 
 /* IntegrationResult, driver.hpp:60-68 (+ timing) */
 typedef struct pagani_result {

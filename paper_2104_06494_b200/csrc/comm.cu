@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -60,8 +61,10 @@ NcclApi& nccl() {
     api.GetErrorString =
         reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
   });
-  if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.Send)
-    throw NcclError("NCCL (libnccl.so.2) is not available");
+  if (!api.h) throw NcclError("NCCL (libnccl.so.2) is not available");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.Send ||
+      !api.Recv || !api.GroupStart || !api.GroupEnd)
+    throw NcclError("libnccl.so.2 lacks an entry point this library uses (need NCCL >= 2.7)");
   return api;
 }
 
@@ -207,8 +210,10 @@ int pagani_comm_init_rank(const uint8_t* unique_id, int nranks, int rank, int de
                           void** comm) {
   return pgn::comm_guard([&] {
     if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank/size");
+    // the communicator first: if ncclCommInitRank throws, nothing leaks
+    std::unique_ptr<pgn::Comm> c(new pgn::NcclComm(unique_id, nranks, rank, device));
     auto* h = new pgn::Handle();
-    h->comm = new pgn::NcclComm(unique_id, nranks, rank, device);
+    h->comm = c.release();
     *comm = h;
   });
 }
@@ -217,8 +222,9 @@ int pagani_comm_init_host(const pagani_host_transport* t, int device, void** com
   return pgn::comm_guard([&] {
     if (!t || !t->allgather || !t->exchange || t->size < 1 || t->rank < 0 || t->rank >= t->size)
       throw std::invalid_argument("bad host transport");
+    std::unique_ptr<pgn::Comm> c(new pgn::HostComm(*t, device));
     auto* h = new pgn::Handle();
-    h->comm = new pgn::HostComm(*t, device);
+    h->comm = c.release();
     *comm = h;
   });
 }

@@ -104,6 +104,7 @@ Workspace::~Workspace() {
   if (h_zc) cudaFreeHost(h_zc);
   if (h_ready) cudaFreeHost(h_ready);
   if (h_kb) cudaFreeHost(h_kb);
+  if (h_kbzc) cudaFreeHost(h_kbzc);
   if (st) cudaStreamDestroy(st);
 }
 
@@ -139,6 +140,10 @@ void Workspace::ensure_shard(int R, int n_, int64_t nb_global, int64_t nblk_max_
   st_len.alloc(static_cast<size_t>(nn) * stage_cap);
   st_pest.alloc(stage_cap);
   if (!h_kb) PGN_CK(cudaMallocHost(&h_kb, (kMaxRanks + 1) * sizeof(int64_t)));
+  if (!h_kbzc) {
+    PGN_CK(cudaHostAlloc(&h_kbzc, (kMaxRanks + 1) * sizeof(int64_t), cudaHostAllocMapped));
+    PGN_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_kbzc), h_kbzc, 0));
+  }
 }
 
 void ShardCtx::set_bounds(std::vector<int64_t> b) {
@@ -540,7 +545,10 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     cap_local = ((nbg + R - 1) / R) * kBlock;
     sh->set_bounds(shard_bounds(M, R));
     ws.ensure(n, cap_local);
-    ws.ensure_shard(R, n, nbg + 1, (nbg + R - 1) / R + 1, 2 * ws.cap);
+    // staging for the children that leave this rank: at most all of its
+    // children, 2 * (local kept) <= 2 * cap_local (not the cached ws.cap, which
+    // may be left over from a larger single-GPU run)
+    ws.ensure_shard(R, n, nbg + 1, (nbg + R - 1) / R + 1, 2 * cap_local);
   } else {
     ws.ensure(n, cap_local);
   }
@@ -645,7 +653,6 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     }
     const size_t k2 = kt.mark();
     const int64_t* offsets = ws.off_eval.p;  // kept offsets, indexed by (global) block
-    const bool zero_copy = !sh;
     if (!sh) {
       launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
                       ws.d_zc, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p, ws.d_ready,
@@ -657,27 +664,27 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       comm->allgather(ws.rec_send.p, ws.rec_recv.p, (sh->nblk_max + 1) * sizeof(BlockRec), st);
       launch_unpack_blocks(st, sh->rb, sh->nblk_max, sh->nblk_global, ws.rec_recv.p, ws.g_part.p,
                            ws.g_cnt.p, ws.g_mm.p, ws.g_err0.p);
+      // zero-copy hand-off as on one GPU: the scalars and the kept bounds at
+      // the rank boundaries go to mapped host memory; k_gather_bounds
+      // publishes the sequence number after both (seq 0 = fence, no publish)
       launch_finalize(st, sh->nblk_global, 4, ws.g_part.p, ws.g_cnt.p, ws.g_off.p, ws.g_scratch.p,
-                      ws.d_sc.p, ws.g_mm.p, ws.g_err0.p);
-      launch_gather_bounds(st, sh->rb, ws.g_off.p, ws.g_cnt.p, sh->nblk_global, ws.g_kb.p);
-      PGN_CK(cudaMemcpyAsync(ws.h_kb, ws.g_kb.p, (R + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                             st));
+                      ws.d_zc, ws.g_mm.p, ws.g_err0.p, ws.d_ready, 0);
+      launch_gather_bounds(st, sh->rb, ws.g_off.p, ws.g_cnt.p, sh->nblk_global, ws.d_kbzc,
+                           ws.d_ready, ++ws.seq);
       out->kernel_launches[PAGANI_K_FINALIZE] += 4;
       offsets = ws.g_off.p;
     }
     const size_t k3 = kt.mark();
     kt.span(PAGANI_K_FOLD, k1, k2);
     kt.span(PAGANI_K_FINALIZE, k2, k3);
-    if (zero_copy) {
-      wait_host_flag(ws.h_ready, ws.seq, st);
-      ws.h_sc[0] = *ws.h_zc;
-    } else {
-      PGN_CK(cudaMemcpyAsync(ws.h_sc, ws.d_sc.p, sizeof(FoldScalars), cudaMemcpyDeviceToHost, st));
-      PGN_CK(cudaStreamSynchronize(st));
-    }
+    wait_host_flag(ws.h_ready, ws.seq, st);
+    ws.h_sc[0] = *ws.h_zc;
     out->d2h_bytes += sizeof(FoldScalars);
-    if (sh)
-      for (int r = 0; r <= R; ++r) kb[r] = ws.h_kb[r];
+    if (sh) {
+      const volatile int64_t* hk = ws.h_kbzc;
+      for (int r = 0; r <= R; ++r) kb[r] = hk[r];
+      out->d2h_bytes += (R + 1) * sizeof(int64_t);
+    }
     const FoldScalars sc = ws.h_sc[0];
     acc_v = sc.sum[0];  // block_sum(estimates)
     acc_e = sc.sum[1];  // block_sum(errors)
@@ -830,17 +837,26 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       m = 2 * kept;
     } else {
       const int64_t sc_cap = ws.stage_cap;
-      launch_split(st, n, m, cap, sc_cap, ws.flag.p, use_t ? 1 : 0, t_accepted,
-                   offsets + sh->rb.first[rank], ws.est.p, ws.err.p, ws.axis.p, ws.low[cur].p,
-                   ws.len[cur].p, ws.st_low.p, ws.st_len.p, ws.st_pest.p, nullptr, kb[rank]);
-      PGN_CK(cudaGetLastError());
-      out->kernel_launches[PAGANI_K_SPLIT] += m > 0;
       const std::vector<int64_t> next = shard_bounds(2 * kept, R);
       std::vector<Piece> sends, recvs;
       exchange_plan(R, rank, kb, next, sends, recvs);
-      std::vector<Transfer> ts, tr;
       double* dlow = ws.low[cur ^ 1].p;
       double* dlen = ws.len[cur ^ 1].p;
+      // the piece that stays on this rank is written straight into the next
+      // batch; only the pieces that change owner go through the staging area
+      SplitWindow win;
+      for (const Piece& p : recvs)
+        if (p.peer == rank) {
+          win.low = dlow, win.len = dlen, win.pest = ws.pest.p, win.cap = cap;
+          win.lo = p.src_off, win.hi = p.src_off + p.count, win.dst = p.dst_off;
+        }
+      launch_split(st, n, m, cap, sc_cap, ws.flag.p, use_t ? 1 : 0, t_accepted,
+                   offsets + sh->rb.first[rank], ws.est.p, ws.err.p, ws.axis.p, ws.low[cur].p,
+                   ws.len[cur].p, ws.st_low.p, ws.st_len.p, ws.st_pest.p, nullptr, kb[rank], win);
+      PGN_CK(cudaGetLastError());
+      out->kernel_launches[PAGANI_K_SPLIT] += m > 0;
+      std::vector<Transfer> ts, tr;
+      double sent = 0.0;
       for (const Piece& p : sends) {
         if (p.peer == rank) continue;
         for (int a = 0; a < n; ++a) {
@@ -848,30 +864,26 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
           ts.push_back({p.peer, ws.st_len.p + a * sc_cap + p.src_off, p.count * sizeof(double)});
         }
         ts.push_back({p.peer, ws.st_pest.p + p.src_off, p.count * sizeof(double)});
+        sent += static_cast<double>(p.count) * (16.0 * n + 8.0);
       }
       for (const Piece& p : recvs) {
-        if (p.peer == rank) {  // stays on this GPU: device-to-device copy
-          for (int a = 0; a < n; ++a) {
-            PGN_CK(cudaMemcpyAsync(dlow + a * cap + p.dst_off, ws.st_low.p + a * sc_cap + p.src_off,
-                                   p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
-            PGN_CK(cudaMemcpyAsync(dlen + a * cap + p.dst_off, ws.st_len.p + a * sc_cap + p.src_off,
-                                   p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
-          }
-          PGN_CK(cudaMemcpyAsync(ws.pest.p + p.dst_off, ws.st_pest.p + p.src_off,
-                                 p.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
-          continue;
-        }
+        if (p.peer == rank) continue;
         for (int a = 0; a < n; ++a) {
           tr.push_back({p.peer, dlow + a * cap + p.dst_off, p.count * sizeof(double)});
           tr.push_back({p.peer, dlen + a * cap + p.dst_off, p.count * sizeof(double)});
         }
         tr.push_back({p.peer, ws.pest.p + p.dst_off, p.count * sizeof(double)});
       }
+      out->kernel_bytes[PAGANI_K_EXCHANGE] += sent;
+      out->kernel_launches[PAGANI_K_EXCHANGE] += !ts.empty() || !tr.empty();
+      const size_t x0 = kt.mark();
       comm->exchange(ts, tr, st);
+      kt.span(PAGANI_K_SPLIT, k4, x0);
+      kt.span(PAGANI_K_EXCHANGE, x0, kt.mark());
       sh->set_bounds(next);
       m = sh->local();
     }
-    kt.span(PAGANI_K_SPLIT, k4, kt.mark());
+    if (!sh) kt.span(PAGANI_K_SPLIT, k4, kt.mark());
     cur ^= 1;
     M = 2 * kept;
     out->regions_generated += M;

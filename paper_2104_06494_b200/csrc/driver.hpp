@@ -81,6 +81,8 @@ struct Workspace {
   DevBuf<ProbeRec> prec_send, prec_recv;
   DevBuf<double> st_low, st_len, st_pest;
   int64_t* h_kb = nullptr;  // pinned [kMaxRanks + 1]
+  int64_t* h_kbzc = nullptr;  // mapped pinned [kMaxRanks + 1]: zero-copy kept bounds
+  int64_t* d_kbzc = nullptr;  // device alias of h_kbzc
   void ensure_shard(int R, int n, int64_t nb_global, int64_t nblk_max_cap, int64_t stage);
   DevBuf<FoldScalars> d_sc;
   DevBuf<unsigned long long> mm_keys;

@@ -11,8 +11,21 @@
 // SAME operation order and the SAME fused/unfused choices as the shipped
 // machine code (read from `objdump -d libm.so.6`), and
 // the same tables (glibc_tables.h, extracted by tools/extract_glibc_tables.py).
-// Bit-equality with the host libm is checked by tests/test_glibc_math.py on
-// the CPU and tests/test_gpu_parity.py on the B200.
+// Bit-equality with the host libm is checked by
+// tests/test_host.py::test_host_glibc_restatement_matches_libm on the CPU and
+// tests/test_gpu_parity.py::test_device_glibc_exp_cos_bit_exact on the B200.
+//
+// Attribution / licence: this is a restatement of GNU C Library code and is
+// distributed under the GNU Lesser General Public License, version 2.1 or
+// later (LGPL-2.1+), like its sources:
+//   * sysdeps/ieee754/dbl-64/e_exp.c, e_exp_data.c -- Copyright (C) 2018-2024
+//     Free Software Foundation, Inc.; originally from ARM's optimized-routines
+//     (Szabolcs Nagy), contributed to glibc under the LGPL.
+//   * sysdeps/ieee754/dbl-64/s_sin.c, sincostab.c, usncs.h -- IBM Accurate
+//     Mathematical Library, Copyright (C) 2001-2024 Free Software Foundation,
+//     Inc.; written by International Business Machines Corp.
+// See https://www.gnu.org/licenses/old-licenses/lgpl-2.1.html.  The rest of
+// this repository is not derived from glibc.
 //
 // Every arithmetic op goes through fp_ops.cuh so nvcc cannot contract it.
 // Round-to-nearest is assumed (glibc switches to it when needed; CUDA always

@@ -424,9 +424,11 @@ constexpr int kFinThreads = 1024;
 // tid % 256 == 0: the tree sums, the last thread: the count) fence their
 // writes at system scope, then one thread publishes the sequence number the
 // host is spinning on.
+// seq == 0: fence only (a later kernel publishes).
 __device__ __forceinline__ void signal_host(unsigned* ready, unsigned seq) {
   if (!ready) return;
   if ((threadIdx.x & 255) == 0 || threadIdx.x == blockDim.x - 1) __threadfence_system();
+  if (seq == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -600,11 +602,11 @@ __device__ __forceinline__ int64_t cta_rank(bool keep, int r, int64_t& carry, in
 }
 
 __global__ void __launch_bounds__(kSplitThreads)
-    k_split(int n, int64_t m, int64_t cap_src, int64_t cap_dst, const uint8_t* __restrict__ flag,
+    k_split(int n, int64_t m, int64_t cap_src, int64_t cap_stage, const uint8_t* __restrict__ flag,
             int use_t, double t, const int64_t* __restrict__ offsets, const double* __restrict__ est,
             const double* __restrict__ err, const uint8_t* __restrict__ axis,
-            const double* __restrict__ low, const double* __restrict__ len, double* dlow,
-            double* dlen, double* dpest, double* dperr, int64_t kbase) {
+            const double* __restrict__ low, const double* __restrict__ len, double* dlow0,
+            double* dlen0, double* dpest0, double* dperr, int64_t kbase, SplitWindow win) {
   __shared__ int s_warp[kSplitThreads / 32];
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlock;
@@ -616,7 +618,13 @@ __global__ void __launch_bounds__(kSplitThreads)
     const int64_t k = cta_rank(keep, r, carry, s_warp);
     if (!keep) continue;
     const int ax = __ldg(axis + j);
-    const int64_t c0 = 2 * (k - kbase);
+    int64_t c0 = 2 * (k - kbase);
+    double *dlow = dlow0, *dlen = dlen0, *dpest = dpest0;
+    int64_t cap_dst = cap_stage;
+    if (win.low && c0 >= win.lo && c0 < win.hi) {  // stays on this rank: straight to the batch
+      dlow = win.low, dlen = win.len, dpest = win.pest, cap_dst = win.cap;
+      c0 += win.dst - win.lo;
+    }
     for (int a = 0; a < n; ++a) {  // geometry.cpp:122-141
       const double lo = __ldg(low + a * cap_src + j);
       const double ln = __ldg(len + a * cap_src + j);
@@ -818,13 +826,22 @@ __global__ void k_unpack_probe(RankBlocks rb, int64_t nblk_max, int64_t nblk_glo
 }
 
 __global__ void k_gather_bounds(RankBlocks rb, const int64_t* offsets, const int64_t* cnt,
-                                int64_t nblk_global, int64_t* out) {
+                                int64_t nblk_global, int64_t* out, unsigned* ready,
+                                unsigned seq) {
   const int r = threadIdx.x;
   if (r < rb.R) out[r] = rb.first[r] < nblk_global ? offsets[rb.first[r]]
                                                     : (nblk_global ? offsets[nblk_global - 1] +
                                                                          cnt[nblk_global - 1]
                                                                    : 0);
   if (r == rb.R) out[r] = nblk_global ? offsets[nblk_global - 1] + cnt[nblk_global - 1] : 0;
+  if (ready) {  // `out` is mapped host memory: fence every write, then publish
+    if (r <= rb.R) __threadfence_system();
+    __syncthreads();
+    if (r == 0) {
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(ready) = seq;
+    }
+  }
 }
 
 }  // namespace
@@ -855,8 +872,9 @@ void launch_unpack_probe(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max
                                                             part, cnt);
 }
 void launch_gather_bounds(cudaStream_t st, const RankBlocks& rb, const int64_t* offsets,
-                          const int64_t* cnt, int64_t nblk_global, int64_t* out) {
-  k_gather_bounds<<<1, kMaxRanks + 1, 0, st>>>(rb, offsets, cnt, nblk_global, out);
+                          const int64_t* cnt, int64_t nblk_global, int64_t* out, unsigned* ready,
+                          unsigned seq) {
+  k_gather_bounds<<<1, kMaxRanks + 1, 0, st>>>(rb, offsets, cnt, nblk_global, out, ready, seq);
 }
 
 const uint64_t* device_exp_table() {
@@ -994,13 +1012,13 @@ void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long lo
 // region issues all 2N + 2 of its loads before any store.
 template <int N>
 __global__ void __launch_bounds__(kSplitThreads)
-    k_split_n(int64_t m, int64_t cap_src, int64_t cap_dst, const uint8_t* __restrict__ flag,
+    k_split_n(int64_t m, int64_t cap_src, int64_t cap_stage, const uint8_t* __restrict__ flag,
               int use_t, double t, const int64_t* __restrict__ offsets,
               const double* __restrict__ est, const double* __restrict__ err,
               const uint8_t* __restrict__ axis, const double* __restrict__ low,
-              const double* __restrict__ len, double* __restrict__ dlow,
-              double* __restrict__ dlen, double* __restrict__ dpest, double* __restrict__ dperr,
-              int64_t kbase) {
+              const double* __restrict__ len, double* __restrict__ dlow0,
+              double* __restrict__ dlen0, double* __restrict__ dpest0, double* __restrict__ dperr,
+              int64_t kbase, SplitWindow win) {
   constexpr int W = kSplitThreads / 32;
   __shared__ int s_cnt[kSplitPer][W];
   const int64_t b = blockIdx.x;
@@ -1046,7 +1064,13 @@ __global__ void __launch_bounds__(kSplitThreads)
       lo[a] = __ldg(low + a * cap_src + j);
       ln[a] = __ldg(len + a * cap_src + j);
     }
-    const int64_t c0 = 2 * (k - kbase);
+    int64_t c0 = 2 * (k - kbase);
+    double *dlow = dlow0, *dlen = dlen0, *dpest = dpest0;
+    int64_t cap_dst = cap_stage;
+    if (win.low && c0 >= win.lo && c0 < win.hi) {  // stays on this rank: straight to the batch
+      dlow = win.low, dlen = win.len, dpest = win.pest, cap_dst = win.cap;
+      c0 += win.dst - win.lo;
+    }
 #pragma unroll
     for (int a = 0; a < N; ++a) {  // geometry.cpp:122-141
       double2 cl, cn;
@@ -1073,7 +1097,8 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
-                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase) {
+                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase,
+                  const SplitWindow& win) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   const unsigned g = static_cast<unsigned>(nblk);
@@ -1082,7 +1107,7 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
   case NN:                                                                                      \
     k_split_n<NN><<<g, kSplitThreads, 0, st>>>(m, cap_src, cap_dst, flag, use_t, t, offsets, est, \
                                                err, axis, low, len, dlow, dlen, dpest, dperr,    \
-                                               kbase);                                          \
+                                               kbase, win);                                     \
     return;
     PGN_SPLIT_CASE(1) PGN_SPLIT_CASE(2) PGN_SPLIT_CASE(3) PGN_SPLIT_CASE(4) PGN_SPLIT_CASE(5)
     PGN_SPLIT_CASE(6) PGN_SPLIT_CASE(7) PGN_SPLIT_CASE(8) PGN_SPLIT_CASE(9) PGN_SPLIT_CASE(10)
@@ -1091,7 +1116,8 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
 #undef PGN_SPLIT_CASE
     default:
       k_split<<<g, kSplitThreads, 0, st>>>(n, m, cap_src, cap_dst, flag, use_t, t, offsets, est,
-                                           err, axis, low, len, dlow, dlen, dpest, dperr, kbase);
+                                           err, axis, low, len, dlow, dlen, dpest, dperr, kbase,
+                                           win);
   }
 }
 

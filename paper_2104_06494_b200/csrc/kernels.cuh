@@ -97,6 +97,16 @@ void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64
 void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,
                    double* out);
 
+// Sharded runs: children whose (local) index c lies in [lo, hi) stay on this
+// rank and are written straight into the next batch at c - lo + dst (stride
+// cap); the others go to the staging buffers for the exchange.
+struct SplitWindow {
+  double* low = nullptr;
+  double* len = nullptr;
+  double* pest = nullptr;
+  int64_t cap = 0, lo = 0, hi = 0, dst = 0;
+};
+
 // Fused filter (classify.cpp:97-129) + bisect (geometry.cpp:114-143): region
 // j with flag 1 and rank k among the kept writes children 2k, 2k+1 into dst.
 // kbase: subtracted from the (global) kept rank before writing children.
@@ -104,7 +114,8 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
-                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase = 0);
+                  double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase = 0,
+                  const SplitWindow& win = SplitWindow{});
 
 // Compaction only (filter() for the batch API).
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
@@ -162,8 +173,10 @@ void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const dou
 void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
                            const int64_t* cnt, double* scratch, ProbeScalars* out);
 // out[r] = offsets[first_block[r]] (r < R), out[R] = total (from FoldScalars-like count)
+// With `ready`, `out` is mapped host memory and the kernel publishes `seq`.
 void launch_gather_bounds(cudaStream_t st, const RankBlocks& rb, const int64_t* offsets,
-                          const int64_t* cnt, int64_t nblk_global, int64_t* out);
+                          const int64_t* cnt, int64_t nblk_global, int64_t* out,
+                          unsigned* ready = nullptr, unsigned seq = 0);
 
 // Device copies of the glibc tables.
 const uint64_t* device_exp_table();

@@ -345,6 +345,30 @@ def test_integrate_matches_reference_finals_bigcap(pg, gpu):
         assert len(res.threshold_events) == min(want["n_events"], 256), name
 
 
+def test_integrate_matches_10d_traces(pg, gpu):
+    """BASELINE configs[4]'s dimension (f4 Gaussian 10D: N = 1245 rule points,
+    its own k_evaluate instance) over full-length runs of the unmodified
+    reference (tests/golden/traces_10d.json, make_10d_traces.py): every
+    per-iteration field, the threshold events and the final result, bit for
+    bit, at the default cap (tau 1e-3 and configs[4]'s 1e-7) and at 2^24."""
+    cases = load_golden("traces_10d.json")
+    assert cases, "tests/golden/traces_10d.json is empty"
+    for name, case in cases.items():
+        cfg = pg.Config(tau_rel=case["tau"], rel_filtering_enabled=case["fid"] != 1,
+                        max_regions=case["max_regions"])
+        res = pg.integrate(pg.Integrand(case["fid"]), pg.Bounds.unit_cube(case["n"]), cfg,
+                           trace=True)
+        assert_same_result(res, case["result"])
+        assert_same_trace(res.trace, case["trace"], name)
+        want_ev = case["result"]["threshold_events"]
+        assert len(res.threshold_events) == len(want_ev), name
+        for e, w in zip(res.threshold_events, want_ev):
+            assert (e.iteration, e.success, e.batch_size, e.finished_count,
+                    e.discarded_error, e.budget_limit) == (
+                w["iteration"], w["success"], w["batch_size"], w["finished_count"],
+                unhex(w["discarded_error"]), unhex(w["budget_limit"])), name
+
+
 MORE_CASES = [
     ("mapped_xy", 101, 2, 1e-6, True, {}, [1, 1], ([0, 1], [2, 3])),
     ("mapped_f4", 4, 3, 1e-4, True, {}, None, ([-1, 0, 0.25], [1, 2, 0.75])),
