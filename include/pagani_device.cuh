@@ -29,12 +29,20 @@
 //        -I<repo>/include user.cu -L<repo>/paper_2104_06494_b200 -lpagani_b200
 // The kernel and the library must come from the same checkout: the launcher
 // carries sizeof(EvalParams) and the library rejects a mismatch.
+//
+// The kernel is instantiated per dimension (n = 1..PAGANI_DEVICE_MAX_DIM, 16
+// by default, the reference's limit) so the functor inlines with a constant n
+// and its coordinates stay in registers; define PAGANI_DEVICE_MAX_DIM lower
+// to cut compile time.  The kernel also runs the deterministic 2048-block
+// folds in its tail (as the built-ins do), which the sharded multi-GPU path
+// needs.
 #ifndef PAGANI_DEVICE_CUH_
 #define PAGANI_DEVICE_CUH_
 
 #include <cuda_runtime.h>
 
 #include <type_traits>
+#include <utility>
 
 #include "../paper_2104_06494_b200/csrc/evaluate.cuh"
 #include "pagani.hpp"
@@ -59,6 +67,29 @@ struct MathAdapter {  // fn(x, n, Math) seen through the kernel's (x, n, MathTab
   }
 };
 
+#ifndef PAGANI_DEVICE_MAX_DIM
+#define PAGANI_DEVICE_MAX_DIM 16
+#endif
+static_assert(PAGANI_DEVICE_MAX_DIM >= 1 && PAGANI_DEVICE_MAX_DIM <= 16,
+              "PAGANI_DEVICE_MAX_DIM must be in [1, 16]");
+
+template <class K, int N>
+void launch_dim(const pgn::EvalParams& P, const K& k, unsigned grid, const uint64_t* te,
+                const double* ts, cudaStream_t st, int32_t mode) {
+  if (mode == PAGANI_MODE_FAST)
+    pgn::k_evaluate_fn<K, N, 1><<<grid, pgn::kEvalThreads, pgn::kGenericSmem, st>>>(P, te, ts, k);
+  else
+    pgn::k_evaluate_fn<K, N, 0><<<grid, pgn::kEvalThreads, pgn::kGenericSmem, st>>>(P, te, ts, k);
+}
+
+template <class K, int... Ns>
+bool dispatch_dim(int n, const pgn::EvalParams& P, const K& k, unsigned grid, const uint64_t* te,
+                  const double* ts, cudaStream_t st, int32_t mode,
+                  std::integer_sequence<int, Ns...>) {
+  return ((n == Ns + 1 ? (launch_dim<K, Ns + 1>(P, k, grid, te, ts, st, mode), true) : false) ||
+          ...);
+}
+
 template <class K>
 int launch_user_kernel(const void* params, uint32_t params_size, const void* exp_table,
                        const void* sincos_table, void* stream, int64_t m, int32_t mode,
@@ -71,10 +102,9 @@ int launch_user_kernel(const void* params, uint32_t params_size, const void* exp
   const auto* te = static_cast<const uint64_t*>(exp_table);
   const auto* ts = static_cast<const double*>(sincos_table);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (mode == PAGANI_MODE_FAST)
-    pgn::k_evaluate_fn<K, 1><<<grid, pgn::kEvalThreads, 0, st>>>(P, te, ts, k);
-  else
-    pgn::k_evaluate_fn<K, 0><<<grid, pgn::kEvalThreads, 0, st>>>(P, te, ts, k);
+  if (!dispatch_dim(P.n, P, k, grid, te, ts, st, mode,
+                    std::make_integer_sequence<int, PAGANI_DEVICE_MAX_DIM>{}))
+    return static_cast<int>(cudaErrorInvalidValue);  // n > PAGANI_DEVICE_MAX_DIM
   return static_cast<int>(cudaGetLastError());
 }
 

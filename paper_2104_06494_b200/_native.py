@@ -26,7 +26,7 @@ PAGANI_HOST_FN = 1
 PAGANI_MAX_PARAMS = 32
 PAGANI_MAX_EVENTS = 256
 PAGANI_N_KERNEL_SLOTS = 8
-KERNEL_SLOTS = ["evaluate", "fold", "finalize", "minmax", "probe", "split", "init", "other"]
+KERNEL_SLOTS = ["evaluate", "fold", "finalize", "minmax", "probe", "split", "init", "exchange"]
 
 MODE_PARITY = 0
 MODE_FAST = 1

@@ -15,6 +15,7 @@
 // per-iteration trace field with the reference library).
 #include "driver.hpp"
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -130,6 +131,7 @@ void Workspace::ensure_shard(int R, int n_, int64_t nb_global, int64_t nblk_max_
   g_scratch_multi.alloc(2 * 2 * kMaxProbes * nb + 2);
   g_scratch.alloc(2 * nb + 2);
   g_kb.alloc(kMaxRanks + 1);
+  g_val.alloc(kMaxRanks);
   rec_send.alloc(nblk_max_cap + 1);
   rec_recv.alloc(static_cast<size_t>(R) * (nblk_max_cap + 1));
   prec_send.alloc(nblk_max_cap + 1);
@@ -225,6 +227,7 @@ EvalLaunch evaluate_kernel(const DeviceIntegrand& di, int n, int mode) {
     EvalLaunch k;
     k.ext = di.ext;
     k.mode = mode;
+    k.fused_fold = true;  // k_evaluate_fn folds its 2048-blocks (pagani_device.cuh)
     return k;
   }
   return lookup_evaluate(di.fid, n, mode);
@@ -499,10 +502,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   // how the NCCL transport is exercised on a single-GPU host).
   if (comm) {
     if (R > kMaxRanks) throw std::invalid_argument("too many ranks");
-    if (!eval_k.fused_fold)
-      throw UnsupportedError("multi-GPU runs need a builtin separable integrand (f1..f8)");
-    if (cfg.validate_invariants)
-      throw UnsupportedError("validate_invariants is single-GPU only");
+    if (!eval_k.fused_fold)  // only under the PAGANI_UNFUSED_FOLD experiment switch
+      throw UnsupportedError("multi-GPU runs need the evaluate kernel's fused block folds");
     shard.comm = comm;
     shard.R = R;
     shard.rank = comm->rank();
@@ -611,6 +612,24 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   double finished_volume = 0.0;
   std::vector<int64_t> kb(R + 1, 0);  // global kept offsets at rank boundaries
 
+  // validate_invariants on a sharded run: the per-rank values of a check are
+  // allgathered and added in rank order (the checks are tolerances, not
+  // bit-exact quantities; one GPU uses the reference's exact sums).
+  auto global_sum = [&](double* dval) -> double {
+    double hv[kMaxRanks] = {};
+    if (!sh) {
+      PGN_CK(cudaMemcpyAsync(hv, dval, sizeof(double), cudaMemcpyDeviceToHost, st));
+      PGN_CK(cudaStreamSynchronize(st));
+      return hv[0];
+    }
+    comm->allgather(dval, ws.g_val.p, sizeof(double), st);
+    PGN_CK(cudaMemcpyAsync(hv, ws.g_val.p, R * sizeof(double), cudaMemcpyDeviceToHost, st));
+    PGN_CK(cudaStreamSynchronize(st));
+    double tot = 0.0;
+    for (int r = 0; r < R; ++r) tot += hv[r];
+    return tot;
+  };
+
   auto finish = [&](int status, int it) {
     out->status = status;
     out->iterations = it;
@@ -696,9 +715,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
     if (cfg.validate_invariants) {  // driver.cpp:75-79,148
       launch_serial_volume(st, n, m, cap, ws.len[cur].p, nullptr, 0, ws.d_tmp.p);
-      double tv = 0;
-      PGN_CK(cudaMemcpyAsync(&tv, ws.d_tmp.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-      PGN_CK(cudaStreamSynchronize(st));
+      const double tv = global_sum(ws.d_tmp.p);
       if (std::fabs(tv + finished_volume - 1.0) > 1e-10)
         throw std::logic_error("invariant violated: volume not conserved");
     }
@@ -792,10 +809,22 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
         fflag = ws.flag2.p;
       }
       launch_serial_volume(st, n, m, cap, ws.len[cur].p, fflag, 0, ws.d_tmp.p);
-      double fv = 0;
-      PGN_CK(cudaMemcpyAsync(&fv, ws.d_tmp.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-      PGN_CK(cudaStreamSynchronize(st));
-      finished_volume += fv;
+      finished_volume += global_sum(ws.d_tmp.p);
+      // driver.cpp:185-190: the filter conserves the estimate.  kept_v =
+      // block_sum of the kept estimates in compacted order.
+      const int64_t kept_local = sh ? kb[rank + 1] - kb[rank] : kept;
+      const int64_t nbk = nblocks_of(kept_local);
+      if (nbk > 0) {
+        launch_kept_partials(st, m, ws.flag.p, use_t ? 1 : 0, t_accepted, ws.err.p, ws.est.p,
+                             ws.part_probe.p);
+        launch_finalize(st, nbk, 1, ws.part_probe.p, nullptr, nullptr, ws.scratch.p, ws.d_sc.p);
+      } else {
+        PGN_CK(cudaMemsetAsync(ws.d_sc.p, 0, sizeof(FoldScalars), st));
+      }
+      const double kept_v = global_sum(ws.d_sc.p->sum);
+      const double scale = std::max({1e-30, std::fabs(acc_v), std::fabs(fin_v)});
+      if (std::fabs(kept_v + fin_v - acc_v) > 1e-10 * scale)
+        throw std::logic_error("invariant violated: estimate not conserved by filter");
       if (fin_e < 0.0) throw std::logic_error("invariant violated: negative finished error");
     }
 

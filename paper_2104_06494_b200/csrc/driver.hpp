@@ -75,6 +75,7 @@ struct Workspace {
   int64_t nb_global_cap = 0, stage_cap = 0;
   int stage_n = 0;
   DevBuf<double> g_part, g_err0, g_part_multi, g_scratch_multi, g_scratch;
+  DevBuf<double> g_val;  // [kMaxRanks]: per-rank scalars of the validate_invariants checks
   DevBuf<int64_t> g_cnt, g_off, g_off_probe, g_cnt_multi, g_kb;
   DevBuf<unsigned long long> g_mm;
   DevBuf<BlockRec> rec_send, rec_recv;

@@ -11,7 +11,7 @@ namespace pgn {
 
 template <class F>
 static EvalLaunch pick(int mode) {
-  return {mode ? &k_evaluate_gen<F, 1> : &k_evaluate_gen<F, 0>, 0, false};
+  return {mode ? &k_evaluate_gen<F, 1> : &k_evaluate_gen<F, 0>, kGenericSmem, true};
 }
 
 EvalLaunch lookup_eval_f1(int, int);

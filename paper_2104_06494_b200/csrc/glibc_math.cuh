@@ -277,8 +277,93 @@ PGN_HD double gm_do_sin(double x, double dx, const double* __restrict__ SC,
                    (pgn_asu64(xold) & 0x8000000000000000ULL));
 }
 
-// Returns false when |x| >= 105414350 (glibc's __branred range), which the
-// restatement does not cover; callers fall back and lose bit-equality there.
+// ---- __branred: sysdeps/ieee754/dbl-64/branred.c (glibc 2.39) -------------
+// Payne-Hanek style reduction of |x| >= 105414350 by pi/2 with 2/pi in 24-bit
+// digits (toverp).  The shipped routine has no FMA (plain SSE2 in libm.so.6,
+// checked with objdump), so every operation is rounded on its own, in the C
+// source's order.  Returns the quadrant; *a + *aa is the reduced argument.
+#if defined(__CUDACC__)
+static __constant__ uint64_t g_pgn_toverp[75] = PGN_TOVERP_INIT;
+#endif
+static const uint64_t h_pgn_toverp[75] = PGN_TOVERP_INIT;
+
+struct BranredPart {
+  double b, bb, sum;
+};
+
+PGN_HD BranredPart gm_branred_part(double xp, const uint64_t* tov) {
+  constexpr double big = 0x1.8p52, big1 = 0x1.8p54, tm24 = 0x1p-24;
+  double r[6];
+  double sum = 0.0;
+  int k = static_cast<int>((pgn_asu64(xp) >> 52) & 2047);
+  k = (k - 450) / 24;
+  if (k < 0) k = 0;
+  // gor = 2^576 with (24 k) subtracted from its exponent
+  double gor = pgn_asf64(0x63f0000000000000ULL - (static_cast<uint64_t>(k * 24) << 52));
+  for (int i = 0; i < 6; ++i) {
+    r[i] = P_MUL(P_MUL(xp, pgn_asf64(tov[k + i])), gor);
+    gor = P_MUL(gor, tm24);
+  }
+  for (int i = 0; i < 3; ++i) {
+    const double s = P_SUB(P_ADD(r[i], big), big);
+    sum = P_ADD(sum, s);
+    r[i] = P_SUB(r[i], s);
+  }
+  double t = 0.0;
+  for (int i = 0; i < 6; ++i) t = P_ADD(t, r[5 - i]);
+  double bb = P_ADD(P_ADD(P_ADD(P_ADD(P_ADD(P_SUB(r[0], t), r[1]), r[2]), r[3]), r[4]), r[5]);
+  double s = P_SUB(P_ADD(t, big), big);
+  sum = P_ADD(sum, s);
+  t = P_SUB(t, s);
+  const double b = P_ADD(t, bb);
+  bb = P_ADD(P_SUB(t, b), bb);
+  s = P_SUB(P_ADD(sum, big1), big1);
+  sum = P_SUB(sum, s);
+  return {b, bb, sum};
+}
+
+PGN_HD int gm_branred(double x, double* a, double* aa) {
+#if defined(__CUDA_ARCH__)
+  const uint64_t* tov = g_pgn_toverp;
+#else
+  const uint64_t* tov = h_pgn_toverp;
+#endif
+  constexpr double split = 0x1.0000002p27, tm600 = 0x1p-600;
+  constexpr double hp0 = 0x1.921fb54442d18p+0, hp1 = 0x1.1a62633145c07p-54;
+  constexpr double mp1 = 0x1.921fb58p+0, mp2 = -0x1.dde974p-27;
+  x = P_MUL(x, tm600);
+  double t = P_MUL(x, split);  // split x into two 26-bit halves
+  const double x1 = P_SUB(t, P_SUB(t, x));
+  const double x2 = P_SUB(x, x1);
+  const BranredPart p1 = gm_branred_part(x1, tov);
+  const BranredPart p2 = gm_branred_part(x2, tov);
+  double sum = P_ADD(p1.sum, p2.sum);
+  double b = P_ADD(p1.b, p2.b);
+  double bb = pgn_fabs(p1.b) > pgn_fabs(p2.b) ? P_ADD(P_SUB(p1.b, b), p2.b)
+                                               : P_ADD(P_SUB(p2.b, b), p1.b);
+  if (b > 0.5) {
+    b = P_SUB(b, 1.0);
+    sum = P_ADD(sum, 1.0);
+  } else if (b < -0.5) {
+    b = P_ADD(b, 1.0);
+    sum = P_SUB(sum, 1.0);
+  }
+  double s = P_ADD(b, P_ADD(P_ADD(bb, p1.bb), p2.bb));
+  t = P_ADD(P_ADD(P_SUB(b, s), bb), P_ADD(p1.bb, p2.bb));
+  b = P_MUL(s, split);
+  const double t1 = P_SUB(b, P_SUB(b, s));
+  const double t2 = P_SUB(s, t1);
+  b = P_MUL(s, hp0);
+  bb = P_ADD(P_ADD(P_ADD(P_SUB(P_MUL(t1, mp1), b), P_MUL(t1, mp2)), P_MUL(t2, mp1)),
+             P_ADD(P_ADD(P_MUL(t2, mp2), P_MUL(s, hp1)), P_MUL(t, hp0)));
+  s = P_ADD(b, bb);
+  t = P_ADD(P_SUB(b, s), bb);
+  *a = s;
+  *aa = t;
+  return static_cast<int>(sum) & 3;  // quadrant
+}
+
+// True when |x| < 105414350 (reduce_sincos range; __branred beyond).
 PGN_HD bool gm_cos_in_range(double x) {
   const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
   return k < 0x419921fbu;
@@ -306,13 +391,11 @@ PGN_HD double gm_cos(double x, const double* __restrict__ SC, const CosK& KC = C
     const double r = (n & 1) ? gm_do_sin(b, db, SC, KC) : gm_do_cos(b, db, SC, KC);
     return ((n + 1) & 2) ? -r : r;
   }
-  if (k < 0x7ff00000u) {
-    // __branred territory (|x| >= 105414350): not restated.
-#if defined(__CUDA_ARCH__)
-    return ::cos(x);
-#else
-    return std::cos(x);
-#endif
+  if (k < 0x7ff00000u) {  // |x| >= 105414350: __branred, then do_sincos(a, da, n + 1)
+    double a, da;
+    const int m = gm_branred(x, &a, &da) + 1;
+    const double r = (m & 1) ? gm_do_cos(a, da, SC, KC) : gm_do_sin(a, da, SC, KC);
+    return (m & 2) ? -r : r;
   }
   return P_DIV(x, x);  // inf or nan -> nan
 }
@@ -384,7 +467,7 @@ PGN_HD double gm_cos_bf(double x, const double* __restrict__ SC) {
   const double rT = P_ADD(a, tt);
   r = (!is_cos && aa < PGN_C(kTaylorMax)) ? rT : r;
   r = neg ? -r : r;
-  // rare: |x| < 2^-27 -> 1; |x| >= 105414350 (not restated) / inf / nan
+  // rare: |x| < 2^-27 -> 1; |x| >= 105414350 (__branred) / inf / nan
   if (k < 0x3e400000u) r = 1.0;
   if (k >= 0x419921fbu) r = gm_cos(x, SC);
   return r;
@@ -558,6 +641,16 @@ __device__ __forceinline__ double gm_do_sin_s(double x, double dx, SmemTab SC, c
   return pgn_asf64((pgn_asu64(r) & 0x7fffffffffffffffULL) | xsign);
 }
 
+// |x| >= 105414350 off the hot path: out of line, so the evaluator's register
+// allocation and instruction footprint do not carry the reduction.
+static __device__ __noinline__ double gm_cos_big_s(double x, SmemTab SC) {
+  double a, da;
+  const int m = gm_branred(x, &a, &da) + 1;
+  const CosK KC{};
+  const double r = (m & 1) ? gm_do_cos_s(a, da, SC, KC) : gm_do_sin_s(a, da, SC, KC);
+  return (m & 2) ? -r : r;
+}
+
 __device__ __forceinline__ double gm_cos_s(double x, SmemTab SC, const CosK& KC) {
   const uint32_t k = static_cast<uint32_t>(pgn_asu64(x) >> 32) & 0x7fffffffu;
   if (k - 0x400368fdu < 0x419921fbu - 0x400368fdu) {  // 2.426265 <= |x| < 105414350
@@ -580,8 +673,8 @@ __device__ __forceinline__ double gm_cos_s(double x, SmemTab SC, const CosK& KC)
     const double da = P_ADD(P_SUB(y, a), PGN_C(kHp1));
     return gm_do_sin_s(a, da, SC, KC);
   }
-  if (k < 0x7ff00000u) return ::cos(x);  // __branred territory: not restated
-  return P_DIV(x, x);                    // inf or nan -> nan
+  if (k < 0x7ff00000u) return gm_cos_big_s(x, SC);  // |x| >= 105414350: __branred
+  return P_DIV(x, x);                               // inf or nan -> nan
 }
 // cos of two independent arguments (f1): the reduce_sincos reductions of both
 // points run as straight-line code (interleaved chains); do_sin / do_cos stay

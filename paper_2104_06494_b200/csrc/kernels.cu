@@ -724,9 +724,27 @@ __global__ void k_serial_volume(int n, int64_t m, int64_t cap, const double* len
   *out = s;
 }
 
+// validate_invariants: the kept regions' estimates in compacted order, summed
+// serially inside 2048-element blocks of that order (reduce.cpp:13-27's
+// leaves; the tree runs in k_finalize).  Debug path: one thread.
+__global__ void k_kept_partials(int64_t m, const uint8_t* flag, int use_t, double t,
+                                const double* err, const double* est, double* part) {
+  double s = 0.0;
+  int64_t c = 0;
+  for (int64_t j = 0; j < m; ++j) {
+    if (!flag[j] || (use_t && err[j] < t)) continue;
+    s = P_ADD(s, est[j]);
+    if (++c % kBlock == 0) {
+      part[c / kBlock - 1] = s;
+      s = 0.0;
+    }
+  }
+  if (c % kBlock) part[c / kBlock] = s;
+}
+
 __global__ void k_math(int which, int64_t m, const double* x, double* y) {
-  __shared__ uint64_t s_exp[256];
-  __shared__ double s_sc[440];
+  __shared__ __align__(16) uint64_t s_exp[256];
+  __shared__ __align__(16) double s_sc[440];
   load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
@@ -738,8 +756,8 @@ __global__ void k_math(int which, int64_t m, const double* x, double* y) {
 
 template <class F>
 __global__ void k_call(int n, int64_t m, const double* x, IntegrandParams ip, double* y) {
-  __shared__ uint64_t s_exp[256];
-  __shared__ double s_sc[440];
+  __shared__ __align__(16) uint64_t s_exp[256];
+  __shared__ __align__(16) double s_sc[440];
   load_tables(s_exp, s_sc, g_exp_tab, reinterpret_cast<const double*>(g_sincos_tab));
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= m) return;
@@ -1148,6 +1166,10 @@ void launch_apply_threshold(cudaStream_t st, int64_t m, const double* err, doubl
 void launch_serial_volume(cudaStream_t st, int n, int64_t m, int64_t cap, const double* len,
                           const uint8_t* flag, int which, double* out) {
   k_serial_volume<<<1, 1, 0, st>>>(n, m, cap, len, flag, which, out);
+}
+void launch_kept_partials(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, double t,
+                          const double* err, const double* est, double* part) {
+  k_kept_partials<<<1, 1, 0, st>>>(m, flag, use_t, t, err, est, part);
 }
 void launch_math(cudaStream_t st, int which, int64_t m, const double* x, double* y) {
   if (m > 0) k_math<<<grid_for(m, 256), 256, 0, st>>>(which, m, x, y);

@@ -133,6 +133,9 @@ void launch_apply_threshold(cudaStream_t st, int64_t m, const double* err, doubl
                             uint8_t* flags);
 void launch_serial_volume(cudaStream_t st, int n, int64_t m, int64_t cap, const double* len,
                           const uint8_t* flag, int which, double* out);
+// Serial 2048-block partials of the kept estimates in compacted order.
+void launch_kept_partials(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, double t,
+                          const double* err, const double* est, double* part);
 void launch_math(cudaStream_t st, int which, int64_t m, const double* x, double* y);
 void launch_call_integrand(cudaStream_t st, int fid, int n, int64_t m, const double* x,
                            const IntegrandParams& ip, double* y);

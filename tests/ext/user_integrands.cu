@@ -43,10 +43,11 @@ struct Product {
 
 template <class Fn>
 int run(const Fn& fn, int n, double tau, int relf, int mode, const double* lower,
-        const double* upper, double* out_d, int64_t* out_i) {
+        const double* upper, double* out_d, int64_t* out_i, void* comm = nullptr) {
   try {
     auto f = pagani::device_integrand(fn);
     pagani::Config cfg;
+    cfg.comm = comm;
     cfg.tau_rel = tau;
     cfg.rel_filtering_enabled = relf != 0;
     cfg.mode = mode ? pagani::Mode::Fast : pagani::Mode::Parity;
@@ -85,6 +86,19 @@ int user_integrate(int which, const double* params, int n, double tau, int relf,
     case 0: return run(Gauss{params[0], params[1]}, n, tau, relf, mode, lower, upper, out_d, out_i);
     case 1: return run(Oscillatory{}, n, tau, relf, mode, lower, upper, out_d, out_i);
     case 2: return run(Product{}, n, tau, relf, mode, lower, upper, out_d, out_i);
+    default: return -1;
+  }
+}
+
+// The same, sharded over the ranks of `comm` (pagani_comm_init_rank / _host).
+int user_integrate_comm(int which, const double* params, int n, double tau, int relf,
+                        void* comm, double* out_d, int64_t* out_i) {
+  switch (which) {
+    case 0:
+      return run(Gauss{params[0], params[1]}, n, tau, relf, 0, nullptr, nullptr, out_d, out_i,
+                 comm);
+    case 1: return run(Oscillatory{}, n, tau, relf, 0, nullptr, nullptr, out_d, out_i, comm);
+    case 2: return run(Product{}, n, tau, relf, 0, nullptr, nullptr, out_d, out_i, comm);
     default: return -1;
   }
 }

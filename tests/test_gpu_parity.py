@@ -65,8 +65,11 @@ def test_device_glibc_exp_cos_bit_exact(pg, gpu, ref):
                               -np.inf, np.nan, -512.0, 1e-300]])),
             (pg.glibc_cos, ref.lib.ref_libm_cos,
              np.concatenate([rng.uniform(-40, 40, 2_000_000), rng.uniform(0, 140, 2_000_000),
+                             # __branred territory (|x| >= 105414350), every binade
+                             np.ldexp(rng.uniform(-2.0, 2.0, 400_000),
+                                      rng.integers(27, 1024, 400_000)),
                              [0.0, -0.0, 1e-9, 0.855469, 2.426265, np.pi / 2, 36.0, np.inf,
-                              np.nan]]))):
+                              np.nan, 105414350.0, 1e22, 1.7976931348623157e308]]))):
         got = fn(xs, on_device=True)
         want = np.empty_like(xs)
         libm(C.c_int64(len(xs)), xs.ctypes.data_as(C.POINTER(C.c_double)),
@@ -427,11 +430,27 @@ def test_driver_known_answers(pg, gpu):
                      pg.Config(init_subdiv=100, max_regions=1000))
 
 
-def test_validate_invariants_mode(pg, gpu, ref):
-    cfg, rcfg = cfg_pair(pg, 1e-3, True, validate_invariants=True)
-    res = pg.integrate(pg.integrand_by_id("f3"), pg.Bounds.unit_cube(3), cfg)
-    want = ref.integrate(3, 3, rcfg)
-    assert (res.estimate, res.iterations) == (want.estimate, want.iterations)
+VALIDATE_CASES = [(3, 3, 1e-3), (4, 3, 1e-6), (2, 4, 1e-4), (5, 5, 1e-4), (6, 3, 1e-5),
+                  (4, 5, 1e-3)]  # the last one trips the reference's own volume check
+
+
+def _outcome(fn):
+    try:
+        r = fn()
+        return ("ok", r.estimate, r.errorest, str(r.status), r.iterations, r.regions_generated)
+    except AssertionError as e:  # logic_error: an invariant tripped
+        return ("logic_error", str(e))
+
+
+@pytest.mark.parametrize("fid,n,tau", VALIDATE_CASES)
+def test_validate_invariants_mode(pg, gpu, ref, fid, n, tau):
+    """validate_invariants (driver.cpp:75-79,148,185-198): volume conservation,
+    filter estimate conservation, finished-error checks.  Same outcome as the
+    reference: identical results, or the same invariant violation."""
+    cfg, rcfg = cfg_pair(pg, tau, True, validate_invariants=True)
+    got = _outcome(lambda: pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n), cfg))
+    want = _outcome(lambda: ref.integrate(fid, n, rcfg))
+    assert got == want
 
 
 def test_determinism_and_workspace_reuse(pg, gpu):

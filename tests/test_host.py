@@ -93,6 +93,18 @@ def test_host_glibc_restatement_matches_libm(pg, ref):
     assert np.array_equal(bits(mine), bits(libm))
     # the branch-free SIMT variant (f1's fin) is the same function
     assert np.array_equal(bits(pg.glibc_cos(cs, on_device=False, branch_free=True)), bits(libm))
+    # __branred territory (|x| >= 105414350): every binade up to DBL_MAX
+    big = np.concatenate([rng.uniform(1.05e8, 1e9, 100_000),
+                          np.ldexp(rng.uniform(1.0, 2.0, 200_000), rng.integers(27, 1024, 200_000)),
+                          np.array([105414350.0, 105414349.99999999, 1e22, 1.7976931348623157e308,
+                                    2.0 ** 1023, 3.0 * 2 ** 600, 8.0e16])])
+    big = np.concatenate([big, -big])
+    want_big = np.empty_like(big)
+    ref.lib.ref_libm_cos(C.c_int64(len(big)), big.ctypes.data_as(C.POINTER(C.c_double)),
+                         want_big.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(bits(pg.glibc_cos(big, on_device=False)), bits(want_big))
+    assert np.array_equal(bits(pg.glibc_cos(big, on_device=False, branch_free=True)),
+                          bits(want_big))
     sweep = np.arange(-20.0, 20.0, 2.5e-6)  # every quadrant / table boundary, densely
     want = np.empty_like(sweep)
     ref.lib.ref_libm_cos(C.c_int64(len(sweep)), sweep.ctypes.data_as(C.POINTER(C.c_double)),
