@@ -284,6 +284,25 @@ int pagani_check_termination(double v, double e, double v_f, double e_f, double 
 int pagani_digits_converged(double v_prev, double v_curr, int digits);
 int pagani_convergence_digits(double tau_rel);
 
+/* integrate_sequential (sequential.hpp:15-18, sequential.cpp:45-139): the
+ * reference's globally adaptive comparison engine (Alg. 1) -- one region per
+ * step from a max-error heap -- with each step's two children evaluated and
+ * refined on the GPU.  Bit-identical to the reference.  mode: PAGANI_MODE_*.
+ * out->iterations = steps; status CONVERGED or MAX_ITERATIONS (eval budget). */
+int pagani_integrate_sequential(const pagani_integrand* f, int ndim, const double* lower,
+                                const double* upper, double tau_rel, double tau_abs,
+                                int64_t max_evals, int32_t validate_invariants, int32_t device,
+                                int32_t mode, pagani_result* out);
+
+/* Reference value of suite integrand `id` ("f1".."f8") in dimension n
+ * (integrands.cpp:178-188 reference_for, long double, bit-identical).
+ * flags: PAGANI_REFVAL_CORRECTED clamps f6's cut-off to the cube (the
+ * reference does not, integrands.cpp:133-140); PAGANI_REFVAL_EXTENDED allows
+ * f8 outside n in {2,3,8} (values from the reference's golden_box_values). */
+#define PAGANI_REFVAL_CORRECTED 1
+#define PAGANI_REFVAL_EXTENDED 2
+int pagani_reference_value(const char* id, int n, int32_t flags, double* out);
+
 /* glibc-exact math used by the device integrands, exported for verification.
  * exp: on_device 0 = host build of the same source, 1 = GPU.
  * cos: 0 = host gm_cos, 1 = GPU gm_cos, 2 = GPU branch-free gm_cos_bf (used by

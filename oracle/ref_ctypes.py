@@ -318,9 +318,10 @@ class Ref(_Lib):
         return self.fn("reference_value")(fid_name.encode(), C.c_int(dim))
 
     def integrate_sequential(self, fid, ndim, tau_rel, tau_abs=1e-20, max_evals=10_000_000,
-                             params=None):
+                             params=None, lower=None, upper=None):
         p, npar = _params(params)
-        lo, hi = np.zeros(ndim), np.ones(ndim)
+        lo = np.zeros(ndim) if lower is None else np.asarray(lower, dtype=np.float64)
+        hi = np.ones(ndim) if upper is None else np.asarray(upper, dtype=np.float64)
         out = RefResult()
         self._check(self.fn("integrate_sequential")(
             fid, _dp(p), npar, ndim, _dp(lo), _dp(hi), C.c_double(tau_rel),

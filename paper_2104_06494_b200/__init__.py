@@ -8,7 +8,7 @@ from .api import (Bounds, Config, FilterResult, IntegrationResult, Integrand, Re
                   Status, ThresholdEvent, ThresholdLimits, ThresholdResult, apply_threshold,
                   bisect, block_sum, block_sum_where, build_rule, check_termination,
                   count_flags, device_count, digits_converged, evaluate_batch, filter,
-                  glibc_cos, glibc_exp, initial_subdivisions, integrand_by_id, integrate,
+                  glibc_cos, glibc_exp, initial_subdivisions, integrand_by_id, integrate, integrate_sequential,
                   known_integrand, min_max, rel_err_classify, release, rule_point_count,
                   threshold_classify, to_string, two_level_refine, uniform_split)
 from .suite import IntegrandSpec, reference_value, suite
@@ -18,7 +18,7 @@ __all__ = [
     "Status", "ThresholdEvent", "ThresholdLimits", "ThresholdResult", "apply_threshold",
     "bisect", "block_sum", "block_sum_where", "build_rule", "check_termination", "count_flags",
     "device_count", "digits_converged", "evaluate_batch", "filter", "glibc_cos", "glibc_exp",
-    "initial_subdivisions", "integrand_by_id", "integrate", "known_integrand", "min_max",
+    "initial_subdivisions", "integrand_by_id", "integrate", "integrate_sequential", "known_integrand", "min_max",
     "rel_err_classify", "release", "rule_point_count", "threshold_classify", "to_string",
     "two_level_refine", "uniform_split", "IntegrandSpec", "reference_value", "suite",
 ]

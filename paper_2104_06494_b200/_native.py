@@ -28,6 +28,9 @@ PAGANI_MAX_EVENTS = 256
 PAGANI_N_KERNEL_SLOTS = 8
 KERNEL_SLOTS = ["evaluate", "fold", "finalize", "minmax", "probe", "split", "init", "exchange"]
 
+PAGANI_REFVAL_CORRECTED = 1
+PAGANI_REFVAL_EXTENDED = 2
+
 MODE_PARITY = 0
 MODE_FAST = 1
 REFINER_TWO_LEVEL = 0
@@ -129,6 +132,9 @@ SIGNATURES = {
     "pagani_release": (C.c_int, []),
     "pagani_integrate": (C.c_int, [C.POINTER(Integrand), C.c_int, _D, _D, C.POINTER(Config),
                                    C.POINTER(Result)]),
+    "pagani_integrate_sequential": (C.c_int, [C.POINTER(Integrand), C.c_int, _D, _D, C.c_double,
+                                              C.c_double, C.c_int64, C.c_int32, C.c_int32,
+                                              C.c_int32, C.POINTER(Result)]),
     "pagani_rule_point_count": (C.c_int64, [C.c_int]),
     "pagani_build_rule": (C.c_int, [C.c_int, _D, _D, _D, _D]),
     "pagani_evaluate_batch": (C.c_int, [C.POINTER(Integrand), C.c_int, C.c_int64, _D, _D, _D,
@@ -154,6 +160,8 @@ SIGNATURES = {
     "pagani_check_termination": (C.c_int, [C.c_double] * 6),
     "pagani_digits_converged": (C.c_int, [C.c_double, C.c_double, C.c_int]),
     "pagani_convergence_digits": (C.c_int, [C.c_double]),
+    "pagani_reference_value": (C.c_int, [C.c_char_p, C.c_int, C.c_int32,
+                                         C.POINTER(C.c_double)]),
     "pagani_math_exp": (C.c_int, [C.c_int64, _D, _D, C.c_int32]),
     "pagani_math_cos": (C.c_int, [C.c_int64, _D, _D, C.c_int32]),
     "pagani_call_integrand": (C.c_int, [C.POINTER(Integrand), C.c_int, C.c_int64, _D, _D]),

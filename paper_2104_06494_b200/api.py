@@ -313,6 +313,33 @@ def integrate(f, bounds: Bounds, config: Optional[Config] = None,
         trace=rows if trace else None)
 
 
+def integrate_sequential(f, bounds: Bounds, tau_rel: float, tau_abs: float = 1e-20,
+                         max_evals: int = 10_000_000, validate_invariants: bool = False,
+                         device: int = 0, mode: str = "parity") -> IntegrationResult:
+    """sequential.hpp:15-18 -- the reference's globally adaptive comparison
+    engine (one max-error region per step), each step's two children
+    evaluated and refined on the GPU; bit-identical to the reference."""
+    fi = _as_integrand(f)
+    cf = fi.to_c()
+    n = bounds.dim()
+    lo = (C.c_double * n)(*bounds.lower)
+    hi = (C.c_double * n)(*bounds.upper)
+    out = N.Result()
+    md = {"parity": N.MODE_PARITY, "fast": N.MODE_FAST}[mode]
+    N.check(_lib().pagani_integrate_sequential(C.byref(cf), n, lo, hi, tau_rel, tau_abs,
+                                               max_evals, int(validate_invariants), device, md,
+                                               C.byref(out)))
+    return IntegrationResult(
+        estimate=out.estimate, errorest=out.errorest, status=Status(out.status),
+        iterations=out.iterations, regions_generated=out.regions_generated,
+        eval_count=out.eval_count, threshold_events=[], wall_ms=out.wall_ms,
+        kernel_ms={k: out.kernel_ms[i] for i, k in enumerate(N.KERNEL_SLOTS)},
+        kernel_launches={k: out.kernel_launches[i] for i, k in enumerate(N.KERNEL_SLOTS)},
+        kernel_bytes={k: out.kernel_bytes[i] for i, k in enumerate(N.KERNEL_SLOTS)},
+        region_evals=out.region_evals, peak_regions=out.peak_regions,
+        h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, device_ms=out.device_ms, trace=None)
+
+
 def check_termination(v, e, v_f, e_f, tau_rel, tau_abs) -> bool:  # driver.hpp:71-72
     return bool(_lib().pagani_check_termination(v, e, v_f, e_f, tau_rel, tau_abs))
 

@@ -7,6 +7,10 @@
 
 #include "driver.hpp"
 
+namespace pgn {
+double suite_reference_value(const std::string& id, int n, bool corrected, bool extended);
+}  // namespace pgn
+
 namespace {
 thread_local std::string g_last_error;
 }  // namespace
@@ -493,6 +497,24 @@ int pagani_digits_converged(double v_prev, double v_curr, int digits) {
 }
 
 int pagani_convergence_digits(double tau_rel) { return pgn::convergence_digits(tau_rel); }
+
+int pagani_integrate_sequential(const pagani_integrand* f, int ndim, const double* lower,
+                                const double* upper, double tau_rel, double tau_abs,
+                                int64_t max_evals, int32_t validate_invariants, int32_t device,
+                                int32_t mode, pagani_result* out) {
+  return guarded([&] {
+    pgn::integrate_sequential(f, ndim, lower, upper, tau_rel, tau_abs, max_evals,
+                              validate_invariants, device, mode, out);
+  });
+}
+
+int pagani_reference_value(const char* id, int n, int32_t flags, double* out) {
+  return guarded([&] {
+    if (!id || !out) throw std::invalid_argument("reference_value: null argument");
+    *out = pgn::suite_reference_value(id, n, (flags & PAGANI_REFVAL_CORRECTED) != 0,
+                                      (flags & PAGANI_REFVAL_EXTENDED) != 0);
+  });
+}
 
 int pagani_math_exp(int64_t m, const double* x, double* y, int32_t on_device) {
   return guarded([&] {

@@ -103,6 +103,11 @@ struct Workspace {
 };
 
 Workspace& workspace_for(int device);
+
+// sequential.cu: integrate_sequential (sequential.cpp:45-139) on the device.
+void integrate_sequential(const pagani_integrand* f, int ndim, const double* lower,
+                          const double* upper, double tau_rel, double tau_abs, int64_t max_evals,
+                          int validate_invariants, int device, int mode, pagani_result* out);
 void release_workspaces();
 
 // Integrand descriptor resolved to a device kernel.

@@ -1,8 +1,8 @@
 """The fixed-parameter test suite (integrands.hpp:26-34, integrands.cpp:83-255).
 
 Support code for true-error reporting (bench / CLI), not part of the hot path.
-Reference values are evaluated in Python double precision from the same closed
-forms the reference evaluates in long double (agreement ~1e-15 relative).
+Reference values come from the library (csrc/suite.cpp): the reference's
+long-double closed forms with the same glibc functions, bit-identical.
 
 `reference_value(id, dim)` reproduces the reference, including its f6 defect
 (integrands.cpp:129-136 does not clamp the cut-off (3+i)/10 to the unit cube,
@@ -11,96 +11,26 @@ so for dim >= 7 it returns the integral over a larger box); pass
 """
 from __future__ import annotations
 
-import math
+import ctypes as C
 from dataclasses import dataclass
 
+from . import _native as N
 from .api import Integrand, integrand_by_id
 
 
-def _ref_f1(n):
-    phase, p = 0.0, 1.0
-    for i in range(1, n + 1):
-        h = 0.5 * i
-        phase += h
-        p *= math.sin(h) / h
-    return math.cos(phase) * p
-
-
-def _ref_f2(n):
-    return (100.0 * math.atan(25.0)) ** n
-
-
-def _ref_f3(n):
-    s = 0.0
-    for mask in range(1 << n):
-        denom, bits = 1.0, 0
-        for i in range(n):
-            if mask & (1 << i):
-                denom += i + 1
-                bits += 1
-        s += (-1.0 if bits % 2 else 1.0) / denom
-    scale = 1.0
-    for i in range(1, n + 1):
-        scale *= float(i) * i
-    return s / scale
-
-
-def _ref_f4(n):
-    return (math.sqrt(math.pi) / 25.0 * math.erf(12.5)) ** n
-
-
-def _ref_f5(n):
-    return ((1.0 - math.exp(-5.0)) / 5.0) ** n
-
-
-def _ref_f6(n, corrected=False):
-    p = 1.0
-    for i in range(1, n + 1):
-        c = (3.0 + i) / 10.0
-        if corrected:
-            c = min(c, 1.0)
-        p *= (math.exp((i + 4) * c) - 1.0) / (i + 4)
-    return p
-
-
-def _sum_sq_moment(d, k):
-    binom = [[0.0] * (k + 1) for _ in range(k + 1)]
-    for i in range(k + 1):
-        binom[i][0] = 1.0
-        for j in range(1, i + 1):
-            binom[i][j] = binom[i - 1][j - 1] + (binom[i - 1][j] if j <= i - 1 else 0.0)
-    g = [1.0 / (2 * j + 1) for j in range(k + 1)]
-    for _ in range(2, d + 1):
-        g = [sum(binom[kk][j] * (1.0 / (2 * j + 1)) * g[kk - j] for j in range(kk + 1))
-             for kk in range(k + 1)]
-    return g[k]
-
-
-_F8 = {2: 2.9285329205389220, 3: 27.531960573226068, 8: 8879.8511754142763}
-
-
-def reference_value(name: str, dim: int, corrected: bool = False) -> float:
-    if dim < 1 or dim > 16:
-        raise ValueError("reference_value: dimension out of range")
-    if name == "f1":
-        return _ref_f1(dim)
-    if name == "f2":
-        return _ref_f2(dim)
-    if name == "f3":
-        return _ref_f3(dim)
-    if name == "f4":
-        return _ref_f4(dim)
-    if name == "f5":
-        return _ref_f5(dim)
-    if name == "f6":
-        return _ref_f6(dim, corrected)
-    if name == "f7":
-        return _sum_sq_moment(dim, 11)
-    if name == "f8":
-        if dim not in _F8:
-            raise ValueError("f8 reference available for n in {2,3,8}")
-        return _F8[dim]
-    raise ValueError("unknown integrand id: " + name)
+def reference_value(name: str, dim: int, corrected: bool = False,
+                    extended: bool = False) -> float:
+    """integrands.cpp:178-188 reference_for: the reference's long-double closed
+    forms, bit-identical (csrc/suite.cpp via pagani_reference_value).
+    corrected: f6 over the unit cube (the reference's ref_f6 is not, n >= 7).
+    extended: f8 beyond n in {2, 3, 8} (the reference's generator tool)."""
+    if not isinstance(name, str):
+        raise ValueError("unknown integrand id")
+    out = C.c_double()
+    flags = (N.PAGANI_REFVAL_CORRECTED if corrected else 0) | (
+        N.PAGANI_REFVAL_EXTENDED if extended else 0)
+    N.check(N.load().pagani_reference_value(name.encode(), dim, flags, C.byref(out)))
+    return out.value
 
 
 @dataclass
