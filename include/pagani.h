@@ -304,9 +304,10 @@ int pagani_integrate_sequential(const pagani_integrand* f, int ndim, const doubl
 int pagani_reference_value(const char* id, int n, int32_t flags, double* out);
 
 /* glibc-exact math used by the device integrands, exported for verification.
- * exp: on_device 0 = host build of the same source, 1 = GPU.
- * cos: 0 = host gm_cos, 1 = GPU gm_cos, 2 = GPU branch-free gm_cos_bf (used by
- * f1), 3 = host gm_cos_bf. */
+ * exp: on_device 0 = host build of the same source, 1 = GPU, 2 = GPU paired
+ * form (gm_exp2_s: x[2i], x[2i+1] as one pair, as the evaluator calls it).
+ * cos: 0 = host gm_cos, 1 = GPU gm_cos, 2 = GPU branch-free gm_cos_bf, 3 =
+ * host gm_cos_bf, 4 = GPU paired form (gm_cos2_s, f1's hot path). */
 int pagani_math_exp(int64_t m, const double* x, double* y, int32_t on_device);
 int pagani_math_cos(int64_t m, const double* x, double* y, int32_t on_device);
 /* Evaluate a builtin integrand at host points (m x n), on the device. */

@@ -215,6 +215,32 @@ inline IntegrationResult integrate(const Integrand& f, const Bounds& bounds, con
   return out;
 }
 
+// sequential.hpp:15-18 -- the reference's globally adaptive comparison engine.
+inline IntegrationResult integrate_sequential(const Integrand& f, const Bounds& bounds,
+                                              double tau_rel, double tau_abs = 1e-20,
+                                              std::int64_t max_evals = 10'000'000,
+                                              bool validate_invariants = false, int device = 0) {
+  pagani_result r;
+  check(pagani_integrate_sequential(&f.desc, bounds.dim(), bounds.lower.data(),
+                                    bounds.upper.data(), tau_rel, tau_abs, max_evals,
+                                    validate_invariants ? 1 : 0, device, PAGANI_MODE_PARITY, &r));
+  IntegrationResult out;
+  out.estimate = r.estimate;
+  out.errorest = r.errorest;
+  out.status = static_cast<Status>(r.status);
+  out.iterations = r.iterations;
+  out.regions_generated = r.regions_generated;
+  out.eval_count = r.eval_count;
+  return out;
+}
+
+// integrands.hpp reference_value (integrands.cpp:178-188), long double.
+inline double reference_value(const std::string& id, int dim) {
+  double v = 0.0;
+  check(pagani_reference_value(id.c_str(), dim, 0, &v));
+  return v;
+}
+
 inline bool check_termination(double v, double e, double v_f, double e_f, double tau_rel,
                               double tau_abs) {
   return pagani_check_termination(v, e, v_f, e_f, tau_rel, tau_abs) != 0;

@@ -584,20 +584,26 @@ def min_max(x):
 
 
 # ---------------------------------------------------------- math check ----
-def glibc_exp(x, on_device=True):
+def glibc_exp(x, on_device=True, paired=False):
+    """glibc exp restatement (host build, or the device variant; paired: the
+    two-point form the evaluator uses, x[2i] and x[2i+1] as one pair)."""
     x = _f64(x)
     y = np.empty_like(x)
-    N.check(_lib().pagani_math_exp(len(x), _dp(x), _dp(y), int(on_device)))
+    code = 2 if (paired and on_device) else int(bool(on_device))
+    N.check(_lib().pagani_math_exp(len(x), _dp(x), _dp(y), code))
     return y
 
 
-def glibc_cos(x, on_device=True, branch_free=False):
-    """glibc cos restatement.  on_device: the evaluator's device variant (the
-    one f1 uses); branch_free: the branch-merged SIMT variant (kept as an
-    alternative, measured slower on B200)."""
+def glibc_cos(x, on_device=True, branch_free=False, paired=False):
+    """glibc cos restatement.  on_device: the evaluator's device variant;
+    paired: its two-point form (f1's hot path); branch_free: the branch-merged
+    SIMT variant (kept as an alternative, measured slower on B200)."""
     x = _f64(x)
     y = np.empty_like(x)
-    code = (2 if on_device else 3) if branch_free else int(bool(on_device))
+    if paired and on_device:
+        code = 4
+    else:
+        code = (2 if on_device else 3) if branch_free else int(bool(on_device))
     N.check(_lib().pagani_math_cos(len(x), _dp(x), _dp(y), code))
     return y
 

@@ -527,7 +527,7 @@ int pagani_math_exp(int64_t m, const double* x, double* y, int32_t on_device) {
     Ctx c;
     pgn::DevBuf<double> dx, dy(m);
     h2d(dx, x, m, c.st);
-    pgn::launch_math(c.st, 0, m, dx.p, dy.p);
+    pgn::launch_math(c.st, on_device == 2 ? 3 : 0, m, dx.p, dy.p);
     d2h(y, dy.p, m, c.st);
     PGN_CK(cudaStreamSynchronize(c.st));
   });
@@ -548,7 +548,7 @@ int pagani_math_cos(int64_t m, const double* x, double* y, int32_t on_device) {
     Ctx c;
     pgn::DevBuf<double> dx, dy(m);
     h2d(dx, x, m, c.st);
-    pgn::launch_math(c.st, on_device == 2 ? 2 : 1, m, dx.p, dy.p);
+    pgn::launch_math(c.st, on_device == 2 ? 2 : (on_device == 4 ? 4 : 1), m, dx.p, dy.p);
     d2h(y, dy.p, m, c.st);
     PGN_CK(cudaStreamSynchronize(c.st));
   });

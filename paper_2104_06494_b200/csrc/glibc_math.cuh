@@ -553,6 +553,40 @@ __device__ __forceinline__ double gm_exp_fix(double x, uint64_t ix, uint32_t abs
   return gm_exp_special(tmp, sbits, ki);  // 512 <= |x| < 1024
 }
 
+// gm_exp_fix as straight-line code with selects (every case computed, the
+// right one kept): the paired exp's fix-ups then cost one pass per warp
+// instead of two divergent scalar passes with nested branches.  f4 in 8D/10D
+// sends many points to the 512 <= |x| < 1024 special case and beyond, which
+// made the divergent form the largest non-FP64 cost of k_evaluate at 10D.
+__device__ __forceinline__ double gm_exp_fix_bf(double x, uint64_t ix, uint32_t abstop,
+                                                double tmp, uint64_t sbits, uint64_t ki) {
+  // 512 <= |x| < 1024: gm_exp_special, both signs of k
+  const double sc_p = pgn_asf64(sbits - (1009ULL << 52));
+  const double y_p = P_MUL(P_FMA(sc_p, tmp, sc_p), 0x1p1009);
+  const double sc_n = pgn_asf64(sbits + (1022ULL << 52));
+  const double st = P_MUL(sc_n, tmp);
+  const double y = P_ADD(sc_n, st);
+  double lo = P_ADD(P_SUB(sc_n, y), st);
+  const double hi = P_ADD(1.0, y);
+  lo = P_ADD(P_ADD(P_SUB(1.0, hi), y), lo);
+  double y2 = P_SUB(P_ADD(hi, lo), 1.0);
+  y2 = y2 == 0.0 ? 0.0 : y2;  // avoid -0.0
+  const double y_n = P_MUL(0x1p-1022, y < 1.0 ? y2 : y);
+  double r = (ki & 0x80000000ULL) == 0 ? y_p : y_n;
+  // |x| >= 1024: -inf -> 0, inf / nan -> 1 + x, else under/overflow
+  const double one_x = P_ADD(1.0, x);
+  const double big = ix == 0xfff0000000000000ULL
+                         ? 0.0
+                         : (abstop >= 0x7ffu ? one_x
+                                             : ((ix >> 63) ? 0.0
+                                                           : pgn_asf64(0x7ff0000000000000ULL)));
+  r = abstop >= 0x409u ? big : r;
+  return static_cast<int32_t>(abstop - 0x3c9u) < 0 ? one_x : r;  // |x| < 2^-54
+}
+
+#ifndef PGN_EXP_FIX_BRANCHY
+#define PGN_EXP_FIX_BRANCHY 1  // 0: straight-line gm_exp_fix_bf (measured 1-6% slower on f4 8D/10D)
+#endif
 __device__ __forceinline__ void gm_exp2_s(double x0, double x1, SmemTab T, const ExpK& K,
                                           double& y0, double& y1) {
   using namespace expc;
@@ -583,10 +617,19 @@ __device__ __forceinline__ void gm_exp2_s(double x0, double x1, SmemTab T, const
   y0 = P_FMA(sc0, tmp0, sc0);
   y1 = P_FMA(sc1, tmp1, sc1);
   const bool f0 = at0 - 0x3c9u >= 0x3fu, f1 = at1 - 0x3c9u >= 0x3fu;
+#if PGN_EXP_FIX_BRANCHY
   if (f0 | f1) {
     if (f0) y0 = gm_exp_fix(x0, ix0, at0, tmp0, sbits0, ki0);
     if (f1) y1 = gm_exp_fix(x1, ix1, at1, tmp1, sbits1, ki1);
   }
+#else
+  if (f0 | f1) {  // one straight-line pass for both points
+    const double z0 = gm_exp_fix_bf(x0, ix0, at0, tmp0, sbits0, ki0);
+    const double z1 = gm_exp_fix_bf(x1, ix1, at1, tmp1, sbits1, ki1);
+    y0 = f0 ? z0 : y0;
+    y1 = f1 ? z1 : y1;
+  }
+#endif
 }
 
 __device__ __forceinline__ void gm_sc4(SmemTab SC, int k, double& sn, double& ssn, double& cs,
@@ -641,6 +684,50 @@ __device__ __forceinline__ double gm_do_sin_s(double x, double dx, SmemTab SC, c
   return pgn_asf64((pgn_asu64(r) & 0x7fffffffffffffffULL) | xsign);
 }
 
+// do_sin and do_cos (s_sin.c) as ONE instruction stream: q = 1 selects do_sin,
+// q = 0 do_cos.  The two routines share their structure -- the same table
+// lookup and polynomials, three FMAs into `cor` with the table values in a
+// different arrangement -- so every operand that differs is chosen by a
+// select and each operation is the one the selected routine performs
+// (identical results, bit for bit).  The lanes of a warp take different
+// quadrants, so the branchy form executed both routines for most warps; this
+// form executes one, plus do_sin's TAYLOR_SIN (|x| < 0.126), also selected.
+#ifndef PGN_COS_MERGED
+#define PGN_COS_MERGED 0  // A/B knob: measured +22% k_evaluate time on f1 8D (B200)
+#endif
+__device__ __forceinline__ double gm_do_sc_s(double x, double dx, bool q, SmemTab SC,
+                                             const CosK& KC) {
+  // TAYLOR_SIN (do_sin, |x| < taylor_max)
+  const double xt = P_MUL(x, x);
+  double p = P_FMA(KC.s5, xt, KC.s4);
+  p = P_FMA(p, xt, KC.s3);
+  p = P_FMA(p, xt, KC.s2);
+  p = P_FMA(p, xt, KC.s1);
+  const double r_taylor = P_ADD(x, P_FMA(xt, P_FMA(p, x, -P_MUL(0.5, dx)), dx));
+  // table-driven core
+  const uint64_t xsign = pgn_asu64(x) & 0x8000000000000000ULL;
+  const double dxs = pgn_xor_sign(dx, q ? (x <= 0) : (x < 0));
+  const double ax = pgn_fabs(x);
+  const double u = P_ADD(PGN_C(kBig), ax);
+  const double xr0 = P_SUB(ax, P_SUB(u, PGN_C(kBig)));
+  const double xr = q ? xr0 : P_ADD(xr0, dxs);              // do_cos folds dx in here
+  const double xx = P_MUL(xr, xr);
+  const double t = P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), q ? dxs : xr);
+  const double s = q ? P_ADD(xr, t) : t;                    // sin: x + (dx + x^3 p)
+  const double cp = P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2)));
+  const double c = q ? P_FMA(xr, dxs, cp) : cp;            // sin: x dx + x^2 q
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  double sn, ssn, cs, ccs;
+  gm_sc4(SC, k, sn, ssn, cs, ccs);
+  const double ms = pgn_xor_sign(s, !q);                    // cos uses -s
+  double cor = P_FMA(ms, q ? ccs : ssn, q ? ssn : ccs);
+  cor = P_FMA(-c, q ? sn : cs, cor);
+  cor = P_FMA(ms, q ? cs : sn, cor);
+  const double r = P_ADD(q ? sn : cs, cor);
+  const double rs = pgn_asf64((pgn_asu64(r) & 0x7fffffffffffffffULL) | xsign);  // copysign
+  return q ? (pgn_fabs(x) < KC.taylor_max ? r_taylor : rs) : r;
+}
+
 // |x| >= 105414350 off the hot path: out of line, so the evaluator's register
 // allocation and instruction footprint do not carry the reduction.
 static __device__ __noinline__ double gm_cos_big_s(double x, SmemTab SC) {
@@ -662,7 +749,11 @@ __device__ __forceinline__ double gm_cos_s(double x, SmemTab SC, const CosK& KC)
     double db = P_FMA(-xn, KC.pp3, P_SUB(y, t2));
     const double b = P_FMA(-xn, KC.pp4, t2);
     db = P_ADD(db, P_FMA(-xn, KC.pp4, P_SUB(t2, b)));
+#if PGN_COS_MERGED
+    const double r = gm_do_sc_s(b, db, (n & 1) != 0, SC, KC);
+#else
     const double r = (n & 1) ? gm_do_sin_s(b, db, SC, KC) : gm_do_cos_s(b, db, SC, KC);
+#endif
     return pgn_xor_sign(r, ((n + 1) & 2) != 0);
   }
   if (k < 0x3e400000u) return 1.0;                         // |x| < 2^-27
@@ -700,8 +791,13 @@ __device__ __forceinline__ void gm_cos2_s(double x0, double x1, SmemTab SC, cons
     const double ba = P_FMA(-xn0, KC.pp4, t2a), bb = P_FMA(-xn1, KC.pp4, t2b);
     dba = P_ADD(dba, P_FMA(-xn0, KC.pp4, P_SUB(t2a, ba)));
     dbb = P_ADD(dbb, P_FMA(-xn1, KC.pp4, P_SUB(t2b, bb)));
+#if PGN_COS_MERGED  // straight-line: ptxas interleaves the two cores
+    const double ra = gm_do_sc_s(ba, dba, (n0 & 1) != 0, SC, KC);
+    const double rb = gm_do_sc_s(bb, dbb, (n1 & 1) != 0, SC, KC);
+#else
     const double ra = (n0 & 1) ? gm_do_sin_s(ba, dba, SC, KC) : gm_do_cos_s(ba, dba, SC, KC);
     const double rb = (n1 & 1) ? gm_do_sin_s(bb, dbb, SC, KC) : gm_do_cos_s(bb, dbb, SC, KC);
+#endif
     y0 = pgn_xor_sign(ra, ((n0 + 1) & 2) != 0);
     y1 = pgn_xor_sign(rb, ((n1 + 1) & 2) != 0);
   } else {

@@ -751,6 +751,16 @@ __global__ void k_math(int which, int64_t m, const double* x, double* y) {
   // the evaluator's hot-path variants (tab_exp / tab_cos: shared-address
   // tables, sign-bit XORs) and the branch-free cos
   const MathTables T = make_tables(s_exp, s_sc);
+  if (which >= 3) {  // the paired forms the evaluator uses: (x[2i], x[2i+1]) as one pair
+    const int64_t j0 = j & ~int64_t{1}, j1 = (j | 1) < m ? (j | 1) : j0;
+    double ya, yb;
+    if (which == 3)
+      tab_exp2(x[j0], x[j1], T, ya, yb);
+    else
+      tab_cos2(x[j0], x[j1], T, ya, yb);
+    y[j] = (j & 1) ? yb : ya;
+    return;
+  }
   y[j] = which == 0 ? tab_exp(x[j], T) : (which == 1 ? tab_cos(x[j], T) : gm_cos_bf(x[j], s_sc));
 }
 

@@ -61,8 +61,11 @@ def test_device_glibc_exp_cos_bit_exact(pg, gpu, ref):
     for fn, libm, xs in (
             (pg.glibc_exp, ref.lib.ref_libm_exp,
              np.concatenate([rng.uniform(-1300, 720, 2_000_000), rng.uniform(-45, 45, 2_000_000),
+                             rng.uniform(-760, -500, 1_000_000),  # f4's special-case band
+                             rng.uniform(500, 720, 200_000), rng.uniform(-1e-15, 1e-15, 100_000),
                              [0.0, -0.0, -745.2, -708.3, -1024.0, -1075.0, 709.8, 710.0, np.inf,
-                              -np.inf, np.nan, -512.0, 1e-300]])),
+                              -np.inf, np.nan, -512.0, 1e-300, -745.1332191019411,
+                              -745.1332191019412, -708.3964185322641, 709.782712893384]])),
             (pg.glibc_cos, ref.lib.ref_libm_cos,
              np.concatenate([rng.uniform(-40, 40, 2_000_000), rng.uniform(0, 140, 2_000_000),
                              # __branred territory (|x| >= 105414350), every binade
@@ -75,6 +78,8 @@ def test_device_glibc_exp_cos_bit_exact(pg, gpu, ref):
         libm(C.c_int64(len(xs)), xs.ctypes.data_as(C.POINTER(C.c_double)),
              want.ctypes.data_as(C.POINTER(C.c_double)))
         assert np.array_equal(bits(got), bits(want))
+        # the paired two-point forms the evaluator runs (incl. their fix-ups)
+        assert np.array_equal(bits(fn(xs, on_device=True, paired=True)), bits(want))
         if fn is pg.glibc_cos:
             assert np.array_equal(bits(pg.glibc_cos(xs, on_device=True, branch_free=True)),
                                   bits(want))

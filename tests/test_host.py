@@ -219,12 +219,14 @@ def _build_cpp_example(tmp_path):
     return exe
 
 
-def test_cpp_mirror_header_compiles_links_and_runs_host_parts(tmp_path):
+def test_cpp_mirror_header_compiles_links_and_runs_host_parts(tmp_path, pg):
     """include/pagani.hpp: reference-style C++ (bfcub:: names via the alias)
     builds against the C ABI and links the in-tree library."""
     exe = _build_cpp_example(tmp_path)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "digits=3 d(8)=3 N(8)=401" in out
+    ref = "%.17g" % pg.reference_value("f4", 5)
+    assert f"reference_value(f4, 5) = {ref}" in out
 
 
 @pytest.mark.gpu
@@ -232,6 +234,7 @@ def test_cpp_mirror_header_integrates_on_gpu(tmp_path):
     exe = _build_cpp_example(tmp_path)
     out = subprocess.run([str(exe), "run"], capture_output=True, text=True, check=True).stdout
     assert "f4 5D: 1.7913125097877638e-06" in out and "converged it=11 regions=7959712" in out
+    assert "sequential f4 3D:" in out
 
 
 def _build_device_example(tmp_path):
