@@ -46,11 +46,11 @@ FIDS = (1, 2, 3, 4, 5, 6)
 # (same config, same outcome), ~5-10 s of reference CPU time per step.  The GPU
 # arm runs the same two calls inside its timed steps and reports its rate on
 # them ("same_sample"), so the GPU/CPU ratio on identical work is derivable.
-CPU_SAMPLE = ((3, 1e-3), (3, 1e-4))
-CPU_SAMPLE_DESC = ("complete integrate() calls f3@1e-3 + f3@1e-4 (8D, suite config: "
-                   "2 of the suite's 24 cases, run to their end)")
-# 1-thread protocol run: the first of the two calls
-CPU_SAMPLE_1T = ((3, 1e-3),)
+CPU_SAMPLE = ((3, 1e-3), (3, 1e-4), (5, 1e-3), (4, 1e-3))
+CPU_SAMPLE_DESC = ("complete integrate() calls f3@1e-3, f3@1e-4, f5@1e-3, f4@1e-3 (8D, suite "
+                   "config: 4 of the suite's 24 cases, run to their end; 31.0M region-evals)")
+# 1-thread protocol run: one call of the sample
+CPU_SAMPLE_1T = ((3, 1e-4),)
 
 
 def dist_env():
@@ -404,7 +404,7 @@ def cpu_desc(cpu, threads):
 def one_thread_rate(ref, make_config):
     e, s = ref_sample(ref, make_config, 1, CPU_SAMPLE_1T)
     return {"value": e / s, "unit": UNIT, "threads": 1,
-            "sample": "complete integrate() call f3@1e-3 (8D, suite config)",
+            "sample": "complete integrate() call f3@1e-4 (8D, suite config)",
             "region_evals": e, "seconds": round(s, 3)}
 
 

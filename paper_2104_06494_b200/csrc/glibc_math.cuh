@@ -515,13 +515,13 @@ __device__ __forceinline__ double gm_exp_s(double x, SmemTab T, const ExpK& K) {
   }
   double kd = P_FMA(x, K.inv_ln2_n, PGN_GM(expc, kShift));
   const uint64_t ki = pgn_asu64(kd);
+  const int idx = 2 * static_cast<int>(ki & 127);
+  uint64_t tail_b, sb;
+  T.ld2u(idx, tail_b, sb);  // early: latency under the reduction
   kd = P_SUB(kd, PGN_GM(expc, kShift));
   double r = P_FMA(kd, K.neg_ln2hi_n, x);
   r = P_FMA(kd, K.neg_ln2lo_n, r);
-  const int idx = 2 * static_cast<int>(ki & 127);
   const uint64_t top = ki << 45;
-  uint64_t tail_b, sb;
-  T.ld2u(idx, tail_b, sb);
   const double tail = pgn_asf64(tail_b);
   const uint64_t sbits = sb + top;
   const double p23 = P_FMA(r, K.c3, K.c2);
@@ -596,15 +596,15 @@ __device__ __forceinline__ void gm_exp2_s(double x0, double x1, SmemTab T, const
   double kd0 = P_FMA(x0, K.inv_ln2_n, PGN_GM(expc, kShift));
   double kd1 = P_FMA(x1, K.inv_ln2_n, PGN_GM(expc, kShift));
   const uint64_t ki0 = pgn_asu64(kd0), ki1 = pgn_asu64(kd1);
+  uint64_t tb0, sb0, tb1, sb1;  // table loads first: latency under the reduction
+  T.ld2u(2 * static_cast<int>(ki0 & 127), tb0, sb0);
+  T.ld2u(2 * static_cast<int>(ki1 & 127), tb1, sb1);
   kd0 = P_SUB(kd0, PGN_GM(expc, kShift));
   kd1 = P_SUB(kd1, PGN_GM(expc, kShift));
   double r0 = P_FMA(kd0, K.neg_ln2hi_n, x0);
   double r1 = P_FMA(kd1, K.neg_ln2hi_n, x1);
   r0 = P_FMA(kd0, K.neg_ln2lo_n, r0);
   r1 = P_FMA(kd1, K.neg_ln2lo_n, r1);
-  uint64_t tb0, sb0, tb1, sb1;
-  T.ld2u(2 * static_cast<int>(ki0 & 127), tb0, sb0);
-  T.ld2u(2 * static_cast<int>(ki1 & 127), tb1, sb1);
   const uint64_t sbits0 = sb0 + (ki0 << 45), sbits1 = sb1 + (ki1 << 45);
   const double p23_0 = P_FMA(r0, K.c3, K.c2), p23_1 = P_FMA(r1, K.c3, K.c2);
   const double tr0 = P_ADD(r0, pgn_asf64(tb0)), tr1 = P_ADD(r1, pgn_asf64(tb1));
@@ -642,13 +642,15 @@ __device__ __forceinline__ double gm_do_cos_s(double x, double dx, SmemTab SC, c
   dx = pgn_xor_sign(dx, x < 0);
   const double ax = pgn_fabs(x);
   const double u = P_ADD(PGN_C(kBig), ax);
+  // table loads issued first (the asm loads stay where they are written), so
+  // their latency overlaps the polynomials instead of stalling the FMAs below
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  double sn, ssn, cs, ccs;
+  gm_sc4(SC, k, sn, ssn, cs, ccs);
   const double xr = P_ADD(P_SUB(ax, P_SUB(u, PGN_C(kBig))), dx);
   const double xx = P_MUL(xr, xr);
   const double s = P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), xr);
   const double c = P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2)));
-  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
-  double sn, ssn, cs, ccs;
-  gm_sc4(SC, k, sn, ssn, cs, ccs);
   double cor = P_FMA(-s, ssn, ccs);
   cor = P_FMA(-c, cs, cor);
   cor = P_FMA(-s, sn, cor);
@@ -669,14 +671,14 @@ __device__ __forceinline__ double gm_do_sin_s(double x, double dx, SmemTab SC, c
   dx = pgn_xor_sign(dx, x <= 0);
   const double ax = pgn_fabs(x);
   const double u = P_ADD(PGN_C(kBig), ax);
+  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
+  double sn, ssn, cs, ccs;
+  gm_sc4(SC, k, sn, ssn, cs, ccs);  // early, as in gm_do_cos_s
   const double xr = P_SUB(ax, P_SUB(u, PGN_C(kBig)));
   const double xx = P_MUL(xr, xr);
   const double s = P_ADD(xr, P_FMA(P_MUL(xr, xx), P_FMA(xx, KC.sn5, KC.sn3), dx));
   const double c =
       P_FMA(xr, dx, P_MUL(xx, P_FMA(xx, P_FMA(xx, KC.cs6, KC.cs4), PGN_C(kCs2))));
-  const int k = static_cast<int>(static_cast<uint32_t>(pgn_asu64(u)) << 2);
-  double sn, ssn, cs, ccs;
-  gm_sc4(SC, k, sn, ssn, cs, ccs);
   double cor = P_FMA(s, ccs, ssn);
   cor = P_FMA(-c, sn, cor);
   cor = P_FMA(s, cs, cor);

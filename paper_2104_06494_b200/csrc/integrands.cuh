@@ -148,7 +148,6 @@ struct F3 {  // (1 + sum (i+1) x_i)^-(n+1)       integrands.cpp:39-43
 struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   static constexpr bool kSeparable = true, kCut = false;
   static constexpr bool kCornerRegs = true;  // evaluate.cuh corner_regs
-  static constexpr bool kPrefer4CtasPerSm = true;  // evaluate.cuh eval_min_blocks
   static constexpr int kMath = 1;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int, double x) {
@@ -185,7 +184,7 @@ struct F5 {  // exp(-10 sum |x-1/2|)             integrands.cpp:54-58
 struct F6 {  // exp(sum (i+5) x_i), 0 outside    integrands.cpp:60-67
   static constexpr bool kSeparable = true, kCut = true;
   static constexpr bool kCornerRegs = true;  // evaluate.cuh corner_regs
-  static constexpr bool kPrefer4CtasPerSm = true;  // (with the corner registers)
+  static constexpr bool kPrefer4CtasPerSm = true;  // evaluate.cuh eval_min_blocks
   static constexpr int kMath = 1;  // 0 none, 1 exp, 2 cos
   PGN_HD static double init() { return 0.0; }
   PGN_HD static double term(int a, double x) { return P_MUL(static_cast<double>(a + 5), x); }

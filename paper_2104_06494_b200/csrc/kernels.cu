@@ -1121,15 +1121,194 @@ __global__ void __launch_bounds__(kSplitThreads)
   }
 }
 
+// ---- k_split_bulk<N>: the same fused filter + bisect, geometry staged by TMA --
+// The kept regions' geometry is a sparse subset of the axis-major store, read
+// at 32-byte sector granularity either way; this form reads each
+// 2048-block's low/len rows densely with 1-D bulk copies (cp.async.bulk, 16 KB
+// per row, completion on an mbarrier) into a 2-stage shared-memory ring -- one
+// axis per stage, the next axis in flight while the current one is written --
+// so the loads never occupy registers or warps.  Threads then build the child
+// pairs of their kept regions from shared memory and store them coalesced.
+// Blocks without a kept region issue no copies.  Used when most regions are
+// kept (the host picks it by the kept fraction); k_split_n otherwise.
+constexpr int kBulkThreads = 256;
+constexpr int kBulkPer = static_cast<int>(kBlock) / kBulkThreads;  // 8 rounds
+constexpr size_t kBulkSmem = 2 * 2 * kBlock * sizeof(double);     // 2 stages x {low, len}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kBulkThreads, 3)
+    k_split_bulk(int64_t m, int64_t cap_src, int64_t cap_stage, const uint8_t* __restrict__ flag,
+                 int use_t, double t, const int64_t* __restrict__ offsets, int64_t kept_end,
+                 const double* __restrict__ est, const double* __restrict__ err,
+                 const uint8_t* __restrict__ axis, const double* __restrict__ low,
+                 const double* __restrict__ len, double* __restrict__ dlow0,
+                 double* __restrict__ dlen0, double* __restrict__ dpest0, int64_t kbase,
+                 SplitWindow win) {
+  constexpr int W = kBulkThreads / 32;
+  extern __shared__ __align__(128) double sbuf[];  // [stage][low | len][kBlock]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_cnt[kBulkPer][W];
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlock;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int cnt = static_cast<int>(m - base < kBlock ? m - base : kBlock);
+  // the block's kept count from the exclusive scan: blocks with none issue
+  // no copies, the others start their first two rows before anything else
+  const int64_t k_first = offsets[b];
+  const int64_t k_next = b + 1 < static_cast<int64_t>(gridDim.x) ? offsets[b + 1] : kept_end;
+  if (k_next == k_first) return;
+  // rows are copied in 16-byte units; the store is allocated in 2048-blocks,
+  // so rounding an odd count up stays inside it
+  const uint32_t row_bytes = static_cast<uint32_t>(((cnt + 1) & ~1) * sizeof(double));
+  auto issue = [&](int a, int st) {  // one thread: rows low[a], len[a] -> stage st
+    mbar_expect_tx(&bar[st], 2 * row_bytes);
+    bulk_g2s(sbuf + (2 * st) * kBlock, low + a * cap_src + base, row_bytes, &bar[st]);
+    bulk_g2s(sbuf + (2 * st + 1) * kBlock, len + a * cap_src + base, row_bytes, &bar[st]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int st = 0; st < 2 && st < N; ++st) issue(st, st);
+  }
+
+  // ranks of the kept regions (as k_split_n)
+  bool keep[kBulkPer];
+  unsigned before[kBulkPer];
+#pragma unroll
+  for (int r = 0; r < kBulkPer; ++r) {
+    const int i = r * kBulkThreads + tid;
+    const int64_t j = base + i;
+    const uint8_t fl = i < cnt ? (flag ? __ldg(flag + j) : uint8_t{1}) : uint8_t{0};
+    const double ev = (use_t && i < cnt) ? __ldg(err + j) : 0.0;
+    keep[r] = fl != 0 && !(use_t && ev < t);  // classify.cpp:63-66
+    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
+    before[r] = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_cnt[r][wid] = __popc(bal);
+  }
+  __syncthreads();  // s_cnt and the barrier initialisation visible to all
+  // child slots: c0 = 2 (k - kbase), routed to the next batch (window) or staging
+  int64_t run = k_first;
+  int64_t c0[kBulkPer];
+  bool inwin[kBulkPer];
+  uint32_t ax_pack[2] = {0u, 0u};
+#pragma unroll
+  for (int r = 0; r < kBulkPer; ++r) {
+    int wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int c = s_cnt[r][w];
+      wbase += w < wid ? c : 0;
+      tot += c;
+    }
+    const int64_t k = run + wbase + before[r];
+    run += tot;
+    int64_t c = 2 * (k - kbase);
+    inwin[r] = win.low && c >= win.lo && c < win.hi;
+    if (inwin[r]) c += win.dst - win.lo;
+    c0[r] = c;
+    if (keep[r]) {
+      const int64_t j = base + r * kBulkThreads + tid;
+      const double e = __ldg(est + j);
+      double* dp = inwin[r] ? win.pest : dpest0;
+      *reinterpret_cast<double2*>(dp + c) = make_double2(e, e);
+      ax_pack[r >> 2] |= static_cast<uint32_t>(__ldg(axis + j)) << (8 * (r & 3));
+    }
+  }
+#pragma unroll 1
+  for (int a = 0; a < N; ++a) {
+    const int st = a & 1;
+    mbar_wait(&bar[st], static_cast<uint32_t>(a >> 1) & 1u);
+    const double* sl = sbuf + (2 * st) * kBlock;
+    const double* sn = sbuf + (2 * st + 1) * kBlock;
+#pragma unroll
+    for (int r = 0; r < kBulkPer; ++r) {
+      if (!keep[r]) continue;
+      const int i = r * kBulkThreads + tid;
+      const double lo = sl[i], ln = sn[i];
+      const int ax = static_cast<int>((ax_pack[r >> 2] >> (8 * (r & 3))) & 0xffu);
+      double2 cl, cn;
+      if (a == ax) {  // geometry.cpp:122-141
+        const double half = P_MUL(ln, 0.5);
+        cl = make_double2(lo, P_ADD(lo, half));
+        cn = make_double2(half, half);
+      } else {
+        cl = make_double2(lo, lo);
+        cn = make_double2(ln, ln);
+      }
+      double* dl = inwin[r] ? win.low : dlow0;
+      double* dn = inwin[r] ? win.len : dlen0;
+      const int64_t capd = inwin[r] ? win.cap : cap_stage;
+      *reinterpret_cast<double2*>(dl + a * capd + c0[r]) = cl;
+      *reinterpret_cast<double2*>(dn + a * capd + c0[r]) = cn;
+    }
+    if (a + 2 < N) {
+      __syncthreads();  // every thread is done with stage st
+      if (tid == 0) issue(a + 2, st);
+    }
+  }
+}
+
 void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
                   double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase,
-                  const SplitWindow& win) {
+                  const SplitWindow& win, bool bulk, int64_t kept_end) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   const unsigned g = static_cast<unsigned>(nblk);
+  if (bulk && offsets && kept_end >= 0 && !dperr && n >= 1 && n <= 16) {
+    switch (n) {
+#define PGN_BULK_CASE(NN)                                                                      \
+  case NN: {                                                                                   \
+    opt_in_smem(reinterpret_cast<const void*>(&k_split_bulk<NN>));                             \
+    k_split_bulk<NN><<<g, kBulkThreads, kBulkSmem, st>>>(m, cap_src, cap_dst, flag, use_t, t,  \
+                                                         offsets, kept_end, est, err, axis,    \
+                                                         low, len, dlow, dlen, dpest, kbase,   \
+                                                         win);                                 \
+    return;                                                                                    \
+  }
+      PGN_BULK_CASE(1) PGN_BULK_CASE(2) PGN_BULK_CASE(3) PGN_BULK_CASE(4) PGN_BULK_CASE(5)
+      PGN_BULK_CASE(6) PGN_BULK_CASE(7) PGN_BULK_CASE(8) PGN_BULK_CASE(9) PGN_BULK_CASE(10)
+      PGN_BULK_CASE(11) PGN_BULK_CASE(12) PGN_BULK_CASE(13) PGN_BULK_CASE(14)
+      PGN_BULK_CASE(15) PGN_BULK_CASE(16)
+#undef PGN_BULK_CASE
+      default: break;
+    }
+  }
   switch (n) {
 #define PGN_SPLIT_CASE(NN)                                                                      \
   case NN:                                                                                      \

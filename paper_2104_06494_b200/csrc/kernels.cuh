@@ -110,12 +110,15 @@ struct SplitWindow {
 // Fused filter (classify.cpp:97-129) + bisect (geometry.cpp:114-143): region
 // j with flag 1 and rank k among the kept writes children 2k, 2k+1 into dst.
 // kbase: subtracted from the (global) kept rank before writing children.
+// bulk: the TMA-staged form (k_split_bulk); it needs the kept offsets and
+// kept_end = the kept rank just past this launch's regions.
 void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
                   const double* err, const uint8_t* axis, const double* low, const double* len,
                   double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase = 0,
-                  const SplitWindow& win = SplitWindow{});
+                  const SplitWindow& win = SplitWindow{}, bool bulk = false,
+                  int64_t kept_end = -1);
 
 // Compaction only (filter() for the batch API).
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,

@@ -56,3 +56,8 @@ def test_reference_sample_runs_suite_calls_to_their_end():
     e, s = bench.ref_sample(ref, make_config, os.cpu_count(), ((3, 1e-3),))
     # f3 8D tau=1e-3 (tests/golden/finals_deep.json): 40979 regions evaluated
     assert e == 40979 and s > 0
+    # the sample's size as described (finals_deep.json region counts)
+    from conftest import load_golden
+    fin = load_golden("finals_deep.json")
+    tot = sum(fin[f"f{f}_8d_{t:g}"]["regions_generated"] for f, t in bench.CPU_SAMPLE)
+    assert f"{tot / 1e6:.1f}M region-evals" in bench.CPU_SAMPLE_DESC

@@ -22,13 +22,49 @@ import paper_2104_06494_b200 as pg  # noqa: E402
 suite = importlib.import_module("paper_2104_06494_b200.suite")
 
 
-def run(name, fid, n, tau, cap):
+GOLDEN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                      "golden")
+
+
+def _unhex(v):
+    return float.fromhex(v) if isinstance(v, str) and v.startswith(("0x", "-0x")) else v
+
+
+def pinned_prefix(rows, fid, n, tau):
+    """Iterations of this run's trace that equal the unmodified reference's
+    full-length trace at the default cap (tests/golden/traces_10d.json), up to
+    the first iteration where the reference's cap-dependent memory trigger
+    fires (after that the runs legitimately differ)."""
+    try:
+        gold = json.load(open(os.path.join(GOLDEN, "traces_10d.json")))
+    except OSError:
+        return None
+    for case in gold.values():
+        if (case["fid"], case["n"], case["tau"], case["max_regions"]) != (fid, n, tau, 1 << 22):
+            continue
+        k = 0
+        for got, want in zip(rows, case["trace"]):
+            if want["trig_memory"]:
+                break
+            if any(got[key] != _unhex(v) for key, v in want.items()):
+                return {"matching_iterations": k, "first_mismatch": got["it"]}
+            k += 1
+        return {"matching_iterations": k, "first_mismatch": None,
+                "pinned_by": "tests/golden/traces_10d.json (cap 2^22)"}
+    return None
+
+
+def run(name, fid, n, tau, cap, check_prefix=False):
     cfg = pg.Config(tau_rel=tau, rel_filtering_enabled=fid != 1, max_regions=cap, profile=True)
     pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n),
                  pg.Config(tau_rel=1e-3, rel_filtering_enabled=fid != 1, max_regions=cap, it_max=2))  # warm
     t0 = time.perf_counter()
     r = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n), cfg)
     wall = time.perf_counter() - t0
+    prefix = None
+    if check_prefix:  # a second, traced run (the timed one above is untraced)
+        rt = pg.integrate(pg.Integrand(fid), pg.Bounds.unit_cube(n), cfg, trace=True)
+        prefix = pinned_prefix(rt.trace, fid, n, tau)
     exact = suite.reference_value(f"f{fid}", n, corrected=True)
     return {"config": name, "f": f"f{fid}", "n": n, "tau": tau, "max_regions": cap,
             "region_store_gb": cap * (32 * n + 27) / 1e9,
@@ -37,7 +73,9 @@ def run(name, fid, n, tau, cap):
             "regions_generated": r.regions_generated, "peak_regions": r.peak_regions,
             "region_evals": r.region_evals, "time_to_result_s": r.device_ms / 1e3,
             "wall_s": wall, "region_evals_per_s": r.region_evals / (r.device_ms / 1e3),
-            "kernel_ms": {k: round(v, 2) for k, v in r.kernel_ms.items()}}
+            "kernel_ms": {k: round(v, 2) for k, v in r.kernel_ms.items()},
+            "kernel_launches": dict(r.kernel_launches),
+            "threshold_events": len(r.threshold_events), "pinned_prefix": prefix}
 
 
 def main():
@@ -46,9 +84,10 @@ def main():
     ap.add_argument("--skip-big", action="store_true")
     a = ap.parse_args()
     rows = [run("configs[0]", 4, 5, 1e-3, 1 << 22), run("configs[2]", 2, 8, 1e-9, 1 << 22),
-            run("configs[3]", 5, 8, 1e-8, 1 << 22), run("configs[3]", 6, 8, 1e-8, 1 << 22)]
+            run("configs[3]", 5, 8, 1e-8, 1 << 22), run("configs[3]", 6, 8, 1e-8, 1 << 22),
+            run("configs[4] at the reference cap", 4, 10, 1e-7, 1 << 22, check_prefix=True)]
     if not a.skip_big:
-        rows.append(run("configs[4]", 4, 10, 1e-7, 1 << a.big_cap))
+        rows.append(run("configs[4]", 4, 10, 1e-7, 1 << a.big_cap, check_prefix=True))
     print(json.dumps(rows, indent=1))
 
 
