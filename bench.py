@@ -178,6 +178,21 @@ def load_reference():
     return Ref(), make_config
 
 
+def comm_info(args, world, comm, rank_clocks):
+    """What the ranks ran over (checkable against NCCL_DEBUG=INFO logs)."""
+    info = {"world_size": world, "sharded": comm is not None,
+            "comm_nranks": getattr(comm, "size", 1) if comm is not None else 1}
+    if world > 1:
+        info["backend"] = args.dist_backend
+        try:
+            import torch
+            info["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+        except Exception:  # noqa: BLE001
+            pass
+        info["per_rank_clocks"] = rank_clocks
+    return info
+
+
 # --------------------------------------------------------------- ours -------
 def run_ours(args, rank, world, local_rank):
     import paper_2104_06494_b200 as pg
@@ -257,6 +272,10 @@ def run_ours(args, rank, world, local_rank):
     barrier_sync()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
+    rank_clocks = [clk]
+    if world > 1:  # every rank's clocks (max-over-ranks timing needs all of them sane)
+        rank_clocks = [None] * world
+        torch.distributed.all_gather_object(rank_clocks, clk)
 
     dev_ms = sum(r.device_ms for st in steps for _, _, r in st)
     region_evals = sum(r.region_evals for st in steps for _, _, r in st)
@@ -366,6 +385,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "clocks": clk,
+        "comm": comm_info(args, world, comm, rank_clocks),
         "same_sample": same,
         "time_to_tolerance_s": {f"{c['f']}@{c['tau']:g}": round(c["time_to_result_s"], 6)
                                 for c in per_case},

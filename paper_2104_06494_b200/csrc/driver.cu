@@ -77,6 +77,10 @@ void Workspace::ensure(int n_, int64_t cap_) {
     PGN_CK(cudaMallocHost(&h_mm, 4 * sizeof(double)));
     d_probe.alloc(1);
     PGN_CK(cudaMallocHost(&h_probe, sizeof(ProbeScalars)));
+    PGN_CK(cudaHostAlloc(&h_probe_zc, sizeof(ProbeScalars), cudaHostAllocMapped));
+    PGN_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_probe_zc), h_probe_zc, 0));
+    probe_done.alloc(1);
+    PGN_CK(cudaMemset(probe_done.p, 0, sizeof(int)));
     PGN_CK(cudaHostAlloc(&h_zc, sizeof(FoldScalars), cudaHostAllocMapped));
     PGN_CK(cudaHostAlloc(&h_ready, 64, cudaHostAllocMapped));
     *reinterpret_cast<volatile unsigned*>(h_ready) = 0;
@@ -102,6 +106,7 @@ Workspace::~Workspace() {
   if (h_sc) cudaFreeHost(h_sc);
   if (h_mm) cudaFreeHost(h_mm);
   if (h_probe) cudaFreeHost(h_probe);
+  if (h_probe_zc) cudaFreeHost(h_probe_zc);
   if (h_zc) cudaFreeHost(h_zc);
   if (h_ready) cudaFreeHost(h_ready);
   if (h_kb) cudaFreeHost(h_kb);
@@ -351,9 +356,12 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
     prepare_probes(ps);
     cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
     if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
+    // zero-copy hand-off of the pass results (as k_finalize's scalars): the
+    // last tree CTA publishes a sequence number into mapped host memory
+    const unsigned seq = ++ws.seq;
     if (!sh) {
       launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
-                         ws.scratch_multi.p, ws.d_probe.p);
+                         ws.scratch_multi.p, ws.d_probe_zc, ws.d_ready, seq, ws.probe_done.p);
     } else {  // local blocks -> allgather of block records -> global trees on every rank
       launch_probe_only(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p);
       launch_pack_probe(st, nblocks_of(m), sh->nblk_max, kMaxProbes, ws.part_multi.p,
@@ -362,15 +370,16 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
       launch_unpack_probe(st, sh->rb, sh->nblk_max, sh->nblk_global, kMaxProbes, ws.prec_recv.p,
                           ws.g_part_multi.p, ws.g_cnt_multi.p);
       launch_finalize_multi(st, sh->nblk_global, kMaxProbes, ws.g_part_multi.p, ws.g_cnt_multi.p,
-                            ws.g_scratch_multi.p, ws.d_probe.p);
+                            ws.g_scratch_multi.p, ws.d_probe_zc, ws.d_ready, seq,
+                            ws.probe_done.p);
     }
     if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
-    PGN_CK(cudaMemcpyAsync(ws.h_probe, ws.d_probe.p, sizeof(ProbeScalars), cudaMemcpyDeviceToHost,
-                           st));
-    PGN_CK(cudaStreamSynchronize(st));
+    wait_host_flag(ws.h_ready, seq, st);
+    *ws.h_probe = *ws.h_probe_zc;
     ++r.passes;
     if (probe_ms) {
       float ms = 0;
+      PGN_CK(cudaEventSynchronize(e1));  // recorded right behind the published kernel
       PGN_CK(cudaEventElapsedTime(&ms, e0, e1));
       *probe_ms += ms;
     }

@@ -71,6 +71,9 @@ struct Workspace {
   DevBuf<int64_t> cnt_multi;
   DevBuf<ProbeScalars> d_probe;
   ProbeScalars* h_probe = nullptr;      // pinned
+  ProbeScalars* h_probe_zc = nullptr;   // mapped: zero-copy pass results
+  ProbeScalars* d_probe_zc = nullptr;   // device alias of h_probe_zc
+  DevBuf<int> probe_done;               // k_finalize_multi's CTA arrival counter
   // multi-GPU (sharded) buffers: global-order block arrays, records, staging
   int64_t nb_global_cap = 0, stage_cap = 0;
   int stage_n = 0;

@@ -330,9 +330,20 @@ __global__ void __launch_bounds__(kProbeThreads)
 template <bool SMEM>
 __global__ void __launch_bounds__(256)
     k_finalize_multi(int64_t nblk, int T, const double* part, const int64_t* cnt, double* scratch,
-                     ProbeScalars* out) {
+                     ProbeScalars* out, unsigned* ready, unsigned seq, int* done) {
   const int id = blockIdx.x;  // 0..2T-1 folds, 2T..3T-1 counts
   const int tid = threadIdx.x;
+  // zero-copy hand-off: `out` is mapped host memory; the last CTA to finish
+  // publishes `seq` once every CTA's field is fenced (no D2H copy + sync)
+  auto publish = [&] {
+    if (!ready || tid != 0) return;
+    __threadfence_system();
+    if (atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1) {
+      *done = 0;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(ready) = seq;
+    }
+  };
   if (id >= 2 * T) {
     __shared__ long long s_c[256];
     const int i = id - 2 * T;
@@ -345,6 +356,7 @@ __global__ void __launch_bounds__(256)
       __syncthreads();
     }
     if (tid == 0) out->count[i] = s_c[0];
+    publish();
     return;
   }
   const int w = id / T, i = id % T;
@@ -353,6 +365,7 @@ __global__ void __launch_bounds__(256)
     extern __shared__ double s_tree[];
     const double v = tree_sum_smem(src, nblk, s_tree, tid, 256);
     if (tid == 0) (w == 0 ? out->err_sum : out->est_sum)[i] = v;
+    publish();
     return;
   }
   double* bufs[2] = {scratch + static_cast<int64_t>(id) * 2 * nblk,
@@ -370,6 +383,7 @@ __global__ void __launch_bounds__(256)
     cur = half + (cur & 1);
   }
   if (tid == 0) (w == 0 ? out->err_sum : out->est_sum)[i] = nblk ? src[0] : 0.0;
+  publish();
 }
 
 // Exclusive scan of one count row (offsets of the accepted probe).
@@ -944,13 +958,16 @@ void opt_in_smem(const void* fn) {
 }
 
 void finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
-                    const int64_t* cnt, double* scratch, ProbeScalars* out) {
+                    const int64_t* cnt, double* scratch, ProbeScalars* out, unsigned* ready,
+                    unsigned seq, int* done) {
   const size_t sm = tree_smem_bytes(nblk, 1);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
     opt_in_smem(reinterpret_cast<const void*>(&k_finalize_multi<true>));
-    k_finalize_multi<true><<<3 * T, 256, sm, st>>>(nblk, T, part, cnt, scratch, out);
+    k_finalize_multi<true><<<3 * T, 256, sm, st>>>(nblk, T, part, cnt, scratch, out, ready, seq,
+                                                   done);
   } else {
-    k_finalize_multi<false><<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out);
+    k_finalize_multi<false><<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out, ready, seq,
+                                                    done);
   }
 }
 
@@ -977,18 +994,20 @@ void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const dou
 }
 
 void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
-                           const int64_t* cnt, double* scratch, ProbeScalars* out) {
-  finalize_multi(st, nblk, T, part, cnt, scratch, out);
+                           const int64_t* cnt, double* scratch, ProbeScalars* out,
+                           unsigned* ready, unsigned seq, int* done) {
+  finalize_multi(st, nblk, T, part, cnt, scratch, out, ready, seq, done);
 }
 
 void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
                         const double* err, const uint8_t* flag, double* part, int64_t* cnt,
-                        double* scratch, ProbeScalars* out) {
+                        double* scratch, ProbeScalars* out, unsigned* ready, unsigned seq,
+                        int* done) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
                                                                         flag, part, cnt);
-  finalize_multi(st, nblk, ts.T, part, cnt, scratch, out);
+  finalize_multi(st, nblk, ts.T, part, cnt, scratch, out, ready, seq, done);
 }
 
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets) {

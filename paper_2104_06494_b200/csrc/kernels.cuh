@@ -88,9 +88,12 @@ void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
 
 // T speculative probes in one pass + their trees; part [2][kMaxProbes][nblk],
 // cnt [kMaxProbes][nblk], scratch 2*3*kMaxProbes*nblk doubles.
+// With `ready`, `out` is mapped host memory and the last tree CTA publishes
+// `seq` there (zero-copy hand-off; `done` = a zeroed device counter).
 void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
                         const double* err, const uint8_t* flag, double* part, int64_t* cnt,
-                        double* scratch, ProbeScalars* out);
+                        double* scratch, ProbeScalars* out, unsigned* ready = nullptr,
+                        unsigned seq = 0, int* done = nullptr);
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets);
 
 // min_max over err (reduce.cpp:74-82).  out[0] = min, out[1] = max, as doubles.
@@ -177,7 +180,8 @@ void launch_unpack_probe(cudaStream_t st, const RankBlocks& rb, int64_t nblk_max
 void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* est,
                        const double* err, const uint8_t* flag, double* part, int64_t* cnt);
 void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
-                           const int64_t* cnt, double* scratch, ProbeScalars* out);
+                           const int64_t* cnt, double* scratch, ProbeScalars* out,
+                           unsigned* ready = nullptr, unsigned seq = 0, int* done = nullptr);
 // out[r] = offsets[first_block[r]] (r < R), out[R] = total (from FoldScalars-like count)
 // With `ready`, `out` is mapped host memory and the kernel publishes `seq`.
 void launch_gather_bounds(cudaStream_t st, const RankBlocks& rb, const int64_t* offsets,
