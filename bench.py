@@ -333,6 +333,35 @@ def run_ours(args, rank, world, local_rank):
             hbm[k] = {"kernel": label, "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                       "frac": gbs / hbm_peak if hbm_peak else None,
                       "bytes_per_step": by / args.steps, "ms_per_step": ms / args.steps}
+    # executed-work view: ncu-counted FP64 operations per region-evaluation
+    # (2 per DFMA, 1 per DMUL / DADD; profiles/r02_executed_flops.json) times
+    # this run's region-evaluations over its CUDA-event time
+    executed = None
+    try:
+        ex = json.load(open(os.path.join(ROOT, "profiles", "r02_executed_flops.json")))
+        per = ex["per_integrand"]
+        ex_fl, ex_per_f = 0.0, {}
+        for fid in sorted({f for f, _ in cases}):
+            k = f"f{fid}"
+            if k not in per:
+                continue
+            ev = sum(r.region_evals for st in steps for f, _, r in st if f == fid)
+            ms = sum(r.kernel_ms["evaluate"] for st in steps for f, _, r in st if f == fid)
+            fl = ev * per[k]["executed_fp64_flops_per_region"]
+            ex_fl += fl
+            if ms > 0:
+                ex_per_f[k] = round(fl / (ms / 1e3) / 1e12, 2)
+        if eval_ms > 0 and ex_fl > 0:
+            ex_t = ex_fl / (eval_ms / 1e3) / 1e12
+            executed = {"tflops": ex_t, "frac": ex_t / peak_tflops if peak_tflops else None,
+                        "tflops_per_integrand": ex_per_f,
+                        "note": "FP64 ops the kernel executes (ncu SASS op counters per region-"
+                                "evaluation, 8D, profiles/r02_executed_flops.json) x this run's "
+                                "region-evaluations / k_evaluate time; fewer than the reference's "
+                                "arithmetic (shared separable terms) and mostly DADD/DMUL (parity "
+                                "forbids fusing), so the DFMA-rate peak is out of reach by design"}
+    except Exception:  # noqa: BLE001
+        executed = None
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_evaluate_summary.json")
     if os.path.exists(prof_path):
@@ -374,6 +403,7 @@ def run_ours(args, rank, world, local_rank):
                                     f"{peak_mhz:.0f} MHz; MEASURED_PEAKS.json has no FP64 entry",
                      "flops_model": "SURVEY.md 8(d) F(f,n), paper_2104_06494_b200/roofline.py",
                      "tflops_per_integrand": per_f,
+                     "executed": executed,
                      "eval_ms": eval_ms / args.steps, "eval_launches": eval_launches // args.steps,
                      "eval_share_of_step": eval_ms / dev_ms if dev_ms else None,
                      "kernel_ms_per_step": {k: round(sum(r.kernel_ms[k] for st in steps

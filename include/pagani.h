@@ -180,7 +180,8 @@ typedef struct pagani_result {
   int64_t regions_generated;
   int64_t eval_count;
   int32_t n_events; /* may exceed PAGANI_MAX_EVENTS; events[] holds the first ones */
-  int32_t reserved0;
+  int32_t probe_fallbacks; /* threshold passes whose streamed sums were too close to the
+                              budget to decide and were re-run with the exact folds */
   pagani_threshold_event events[PAGANI_MAX_EVENTS];
   double wall_ms;                              /* host wall time of the call */
   double kernel_ms[PAGANI_N_KERNEL_SLOTS];     /* CUDA-event time per kernel kind (profile=1) */

@@ -86,7 +86,7 @@ class Result(C.Structure):
     _fields_ = [("estimate", C.c_double), ("errorest", C.c_double),
                 ("status", C.c_int32), ("iterations", C.c_int32),
                 ("regions_generated", C.c_int64), ("eval_count", C.c_int64),
-                ("n_events", C.c_int32), ("reserved0", C.c_int32),
+                ("n_events", C.c_int32), ("probe_fallbacks", C.c_int32),
                 ("events", ThresholdEvent * PAGANI_MAX_EVENTS),
                 ("wall_ms", C.c_double),
                 ("kernel_ms", C.c_double * PAGANI_N_KERNEL_SLOTS),

@@ -192,6 +192,7 @@ class IntegrationResult:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     device_ms: float = 0.0
+    probe_fallbacks: int = 0  # streamed threshold passes re-run exactly
     trace: Optional[list] = None
 
 
@@ -310,7 +311,7 @@ def integrate(f, bounds: Bounds, config: Optional[Config] = None,
         kernel_bytes={k: out.kernel_bytes[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         region_evals=out.region_evals, peak_regions=out.peak_regions,
         h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, device_ms=out.device_ms,
-        trace=rows if trace else None)
+        probe_fallbacks=out.probe_fallbacks, trace=rows if trace else None)
 
 
 def integrate_sequential(f, bounds: Bounds, tau_rel: float, tau_abs: float = 1e-20,

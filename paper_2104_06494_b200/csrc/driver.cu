@@ -239,6 +239,18 @@ EvalLaunch evaluate_kernel(const DeviceIntegrand& di, int n, int mode) {
 }
 
 // PAGANI_SPLIT_BULK=0 selects the per-region-load split kernel (A/B runs).
+// PAGANI_PROBE_STREAM=1: the streamed threshold passes (exact counts, fast
+// sums, exact fold of the accepted threshold only).  Bit-identical results,
+// but measured slower than the exact 15-node passes on B200,
+// so the exact passes are the default.
+bool probe_stream() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_PROBE_STREAM");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int split_bulk_mode() {
   static const int mode = [] {
     const char* e = std::getenv("PAGANI_SPLIT_BULK");
@@ -342,62 +354,160 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
   // thresholds) and the host replays the reference's sequential decisions on
   // the results -- identical outcomes, up to 4 probes per round trip.
   enum Dir { kNone, kTowardMax, kTowardMin };
-  Dir last = kNone;
   const int64_t nblk = nblocks_of(m);
-  bool done = false;
-  while (!done && r.attempts < lim.attempt_limit) {
+  // The walk's state; a pass replays it on a copy and commits the copy.
+  struct Walk {
+    Dir last = kNone;
+    bool done = false;
+    int attempts = 0, direction_changes = 0;
+    double p_max = 0.0, t = 0.0;
+    int accepted = -1;  // node accepted in this pass
+  };
+  Walk w;
+  w.p_max = p_max;
+  w.t = t;
+  // Replay the reference's sequential decisions over one pass's 15 nodes.
+  // fast: the sums are the fast ones -- a comparison within their rounding
+  // bound of the budget is undecidable, and the replay reports it (returns
+  // false) without committing anything.
+  auto replay = [&](const ProbeSet& ps, const ProbeScalars& pr, bool fast, Walk& out) -> bool {
+    Walk v = out;
+    int node = 0;
+    for (;;) {
+      ++v.attempts;
+      const int64_t inactive = s_it - pr.count[node];
+      const bool memory_ok = 2 * inactive > s_it;
+      const double discarded = pr.err_sum[node];
+      const double budget = v.p_max * e_budget;
+      if (fast && memory_ok && std::isfinite(discarded) && std::isfinite(budget) &&
+          std::fabs(discarded - budget) <= 1e-12 * std::fabs(discarded) + 1e-300)
+        return false;  // too close to call on a fast sum
+      if (memory_ok && discarded <= budget) {
+        v.accepted = node;
+        out = v;
+        return true;
+      }
+      const Dir dir = memory_ok ? kTowardMin : kTowardMax;
+      if (v.last != kNone && dir != v.last) {
+        ++v.direction_changes;
+        if (v.direction_changes > lim.direction_change_limit) {
+          v.t = ps.t[node];
+          v.done = true;
+          break;
+        }
+        const double stepped = v.p_max + lim.p_max_step;
+        v.p_max = (stepped < lim.p_max_cap) ? stepped : lim.p_max_cap;  // std::min(cap, p+step)
+      }
+      v.last = dir;
+      const int child = dir == kTowardMax ? 2 * node + 1 : 2 * node + 2;
+      v.t = child < kMaxProbes ? ps.t[child]
+                               : (dir == kTowardMax ? (ps.t[node] + max_err) * 0.5
+                                                    : (ps.t[node] + min_err) * 0.5);
+      if (v.attempts >= lim.attempt_limit) {
+        v.done = true;
+        break;
+      }
+      if (child >= kMaxProbes) break;  // next pass rooted at t
+      node = child;
+    }
+    out = v;
+    return true;
+  };
+  const bool fast_ok = !sh && probe_stream();
+  while (!w.done && w.attempts < lim.attempt_limit) {
     ProbeSet ps{};
     ps.T = kMaxProbes;
-    ps.t[0] = t;
+    ps.t[0] = w.t;
     for (int k = 0; 2 * k + 2 < kMaxProbes; ++k) {
       ps.t[2 * k + 1] = (ps.t[k] + max_err) * 0.5;
       ps.t[2 * k + 2] = (ps.t[k] + min_err) * 0.5;
     }
     prepare_probes(ps);
     cudaEvent_t e0 = ws.event(0), e1 = ws.event(1);
-    if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
-    // zero-copy hand-off of the pass results (as k_finalize's scalars): the
-    // last tree CTA publishes a sequence number into mapped host memory
-    const unsigned seq = ++ws.seq;
-    if (!sh) {
-      launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
-                         ws.scratch_multi.p, ws.d_probe_zc, ws.d_ready, seq, ws.probe_done.p);
-    } else {  // local blocks -> allgather of block records -> global trees on every rank
-      launch_probe_only(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p);
-      launch_pack_probe(st, nblocks_of(m), sh->nblk_max, kMaxProbes, ws.part_multi.p,
-                        ws.cnt_multi.p, ws.prec_send.p);
-      sh->comm->allgather(ws.prec_send.p, ws.prec_recv.p, sh->nblk_max * sizeof(ProbeRec), st);
-      launch_unpack_probe(st, sh->rb, sh->nblk_max, sh->nblk_global, kMaxProbes, ws.prec_recv.p,
-                          ws.g_part_multi.p, ws.g_cnt_multi.p);
-      launch_finalize_multi(st, sh->nblk_global, kMaxProbes, ws.g_part_multi.p, ws.g_cnt_multi.p,
-                            ws.g_scratch_multi.p, ws.d_probe_zc, ws.d_ready, seq,
-                            ws.probe_done.p);
-    }
-    if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
-    wait_host_flag(ws.h_ready, seq, st);
-    *ws.h_probe = *ws.h_probe_zc;
-    ++r.passes;
-    if (probe_ms) {
-      float ms = 0;
-      PGN_CK(cudaEventSynchronize(e1));  // recorded right behind the published kernel
-      PGN_CK(cudaEventElapsedTime(&ms, e0, e1));
-      *probe_ms += ms;
-    }
-    const ProbeScalars& pr = *ws.h_probe;
-    int node = 0;
-    for (;;) {
-      ++r.attempts;
-      const int64_t inactive = s_it - pr.count[node];
-      const bool memory_ok = 2 * inactive > s_it;
-      const double discarded = pr.err_sum[node];
-      if (memory_ok && discarded <= p_max * e_budget) {
+    auto timed_wait = [&](unsigned seq) {
+      if (probe_ms) PGN_CK(cudaEventRecord(e1, st));
+      wait_host_flag(ws.h_ready, seq, st);
+      ++r.passes;
+      if (probe_ms) {
+        float ms = 0;
+        PGN_CK(cudaEventSynchronize(e1));  // recorded right behind the published kernel
+        PGN_CK(cudaEventElapsedTime(&ms, e0, e1));
+        *probe_ms += ms;
+      }
+    };
+    bool decided = false;
+    if (fast_ok) {  // streaming pass: exact counts, fast sums
+      if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
+      const unsigned seq = ++ws.seq;
+      launch_probe_fast(st, m, ps, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
+                        ws.d_probe_zc, ws.d_ready, seq);
+      r.bytes += 9.0 * m;  // flag + err
+      timed_wait(seq);
+      *ws.h_probe = *ws.h_probe_zc;
+      decided = replay(ps, *ws.h_probe, true, w);
+      if (!decided) ++r.exact_fallbacks;
+      if (decided && w.accepted >= 0) {
+        // the accepted threshold's sums exactly: the serial 2048-block folds
+        // under its final flags + the pairwise trees + the kept offsets
+        const int node = w.accepted;
+        if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
+        const unsigned seq2 = ++ws.seq;
+        launch_fold_threshold(st, m, d_est, d_err, d_flag, ps.t[node], ws.part_probe.p,
+                              ws.cnt_probe.p);
+        r.bytes += 17.0 * m;  // flag + err + est
+        launch_finalize(st, nblk, 2, ws.part_probe.p, ws.cnt_probe.p, ws.off_probe.p,
+                        ws.scratch.p, ws.d_zc, nullptr, nullptr, ws.d_ready, seq2);
+        timed_wait(seq2);
+        const FoldScalars fs = *ws.h_zc;
+        if (s_it - fs.count != s_it - ws.h_probe->count[node])
+          throw std::logic_error("threshold search: exact and streamed candidate counts differ");
         r.success = true;
         r.threshold = ps.t[node];
-        r.discarded = discarded;
-        r.budget_limit = p_max * e_budget;
-        r.finished_count = inactive;
+        r.discarded = fs.sum[1];  // sum err where final flag == 0
+        r.fin_v = fs.sum[0];      // sum est where final flag == 0
+        r.budget_limit = w.p_max * e_budget;
+        r.finished_count = s_it - fs.count;
+        r.node = node;
+        r.attempts = w.attempts;
+        r.direction_changes = w.direction_changes;
+        return r;
+      }
+    }
+    if (!decided) {  // the exact pass: the strict folds of every node
+      if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
+      // zero-copy hand-off of the pass results (as k_finalize's scalars): the
+      // last tree CTA publishes a sequence number into mapped host memory
+      const unsigned seq = ++ws.seq;
+      r.bytes += 17.0 * m;  // flag + err + est
+      if (!sh) {
+        launch_probe_multi(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p,
+                           ws.scratch_multi.p, ws.d_probe_zc, ws.d_ready, seq, ws.probe_done.p);
+      } else {  // local blocks -> allgather of block records -> global trees on every rank
+        launch_probe_only(st, m, ps, d_est, d_err, d_flag, ws.part_multi.p, ws.cnt_multi.p);
+        launch_pack_probe(st, nblocks_of(m), sh->nblk_max, kMaxProbes, ws.part_multi.p,
+                          ws.cnt_multi.p, ws.prec_send.p);
+        sh->comm->allgather(ws.prec_send.p, ws.prec_recv.p, sh->nblk_max * sizeof(ProbeRec), st);
+        launch_unpack_probe(st, sh->rb, sh->nblk_max, sh->nblk_global, kMaxProbes,
+                            ws.prec_recv.p, ws.g_part_multi.p, ws.g_cnt_multi.p);
+        launch_finalize_multi(st, sh->nblk_global, kMaxProbes, ws.g_part_multi.p,
+                              ws.g_cnt_multi.p, ws.g_scratch_multi.p, ws.d_probe_zc, ws.d_ready,
+                              seq, ws.probe_done.p);
+      }
+      timed_wait(seq);
+      *ws.h_probe = *ws.h_probe_zc;
+      const ProbeScalars& pr = *ws.h_probe;
+      replay(ps, pr, false, w);
+      if (w.accepted >= 0) {
+        const int node = w.accepted;
+        r.success = true;
+        r.threshold = ps.t[node];
+        r.discarded = pr.err_sum[node];
+        r.budget_limit = w.p_max * e_budget;
+        r.finished_count = s_it - pr.count[node];
         r.fin_v = pr.est_sum[node];
         r.node = node;
+        r.attempts = w.attempts;
+        r.direction_changes = w.direction_changes;
         if (!sh) {
           launch_scan_counts(st, nblk, ws.cnt_multi.p + node * nblk, ws.off_probe.p);
         } else {
@@ -408,30 +518,12 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
         }
         return r;
       }
-      const Dir dir = memory_ok ? kTowardMin : kTowardMax;
-      if (last != kNone && dir != last) {
-        ++r.direction_changes;
-        if (r.direction_changes > lim.direction_change_limit) {
-          t = ps.t[node];
-          done = true;
-          break;
-        }
-        const double stepped = p_max + lim.p_max_step;
-        p_max = (stepped < lim.p_max_cap) ? stepped : lim.p_max_cap;  // std::min(cap, p+step)
-      }
-      last = dir;
-      const int child = dir == kTowardMax ? 2 * node + 1 : 2 * node + 2;
-      t = child < kMaxProbes ? ps.t[child]
-                             : (dir == kTowardMax ? (ps.t[node] + max_err) * 0.5
-                                                  : (ps.t[node] + min_err) * 0.5);
-      if (r.attempts >= lim.attempt_limit) {
-        done = true;
-        break;
-      }
-      if (child >= kMaxProbes) break;  // next pass rooted at t
-      node = child;
     }
   }
+  t = w.t;
+  p_max = w.p_max;
+  r.attempts = w.attempts;
+  r.direction_changes = w.direction_changes;
   r.threshold = t;
   r.budget_limit = p_max * e_budget;
   return r;
@@ -774,10 +866,11 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
           ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, M,
           cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr, sh);
       out->kernel_ms[PAGANI_K_PROBE] += pms;
-      out->kernel_bytes[PAGANI_K_PROBE] += static_cast<double>(tr.passes) * m * 17.0;  // flag, err, est
+      out->kernel_bytes[PAGANI_K_PROBE] += tr.bytes;
       out->kernel_launches[PAGANI_K_PROBE] += (sh ? 5 : 2) * tr.passes + (tr.success ? 1 : 0);
       out->kernel_launches[PAGANI_K_MINMAX] += tr.minmax_launches;
       out->d2h_bytes += tr.passes * sizeof(ProbeScalars);
+      out->probe_fallbacks += tr.exact_fallbacks;
       if (out->n_events < PAGANI_MAX_EVENTS) {
         pagani_threshold_event& ev = out->events[out->n_events];
         ev.iteration = it;

@@ -132,6 +132,8 @@ struct ThresholdOutcome {
   int minmax_launches = 0;  // kernels launched by min_max (0 or 3)
   int passes = 0;           // speculative probe passes (2 kernels + 1 D2H each)
   int node = -1;            // accepted node of the last pass
+  int exact_fallbacks = 0;  // streamed passes too close to call (re-run exactly)
+  double bytes = 0.0;       // algorithmic HBM bytes read by the search's kernels
 };
 
 struct Limits {

@@ -122,12 +122,13 @@ __device__ __forceinline__ int64_t stage_block(FoldSmem& S, const double* __rest
 __global__ void __launch_bounds__(kFoldThreads)
     k_fold_eval(int64_t m, int64_t nblk, const double* __restrict__ est,
                 const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
-                int64_t* cnt) {
+                int64_t* cnt, int use_t, double t) {
   __shared__ FoldSmem S;
   const int64_t b = blockIdx.x;
   const int64_t lo = b * kBlock;
   const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
-  const int64_t active = stage_block(S, est, err, flag, lo, n, true, 0.0, false);
+  // use_t: fold under the final flags of threshold t (classify.cpp:63-66)
+  const int64_t active = stage_block(S, est, err, flag, lo, n, true, t, use_t != 0);
   if ((threadIdx.x & 31) != 0 || threadIdx.x >= 64) {
     if (threadIdx.x == 64) cnt[b] = active;
     return;
@@ -322,6 +323,164 @@ __global__ void __launch_bounds__(kProbeThreads)
       for (int k = pos + 1; k <= 16; ++k) c += S.hist[k];
       cnt[node * nblk + b] = c;
     }
+  }
+}
+
+// ---- fast probe pass -----------------------------------------------------------
+// The threshold search's decisions need, per speculative threshold, the exact
+// candidate count and the discarded error compared against a budget; only
+// the ACCEPTED threshold's sums must be the reference's bits.  So a pass
+// streams flag + err once (9 B/region, HBM-bound) and produces exact counts
+// and fast sums in any order -- per thread, warp shuffles, one finalize CTA.
+// The host treats a comparison as decided when |fast - budget| exceeds the
+// sums' rounding bound (both orders are within gamma_2400 of the true sum of
+// the nonnegative errors), falls back to the exact pass otherwise, and folds
+// the accepted threshold exactly (k_fold_eval under the threshold).
+constexpr int kPfThreads = 256;
+
+__global__ void __launch_bounds__(kPfThreads)
+    k_probe_fast(int64_t m, const ProbeSet ts, const double* __restrict__ err,
+                 const uint8_t* __restrict__ flag, double* part, int64_t* cnt) {
+  constexpr int W = kPfThreads / 32;
+  __shared__ double s_s[16];
+  __shared__ double s_acc[W][kMaxProbes];
+  __shared__ long long s_c[W][kMaxProbes];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < 16) s_s[tid] = ts.s[tid];
+  __syncthreads();
+  double acc[kMaxProbes];
+  int c[kMaxProbes];
+#pragma unroll
+  for (int k = 0; k < kMaxProbes; ++k) {
+    acc[k] = 0.0;
+    c[k] = 0;
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kPfThreads;
+#pragma unroll 4
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kPfThreads + tid; j < m; j += stride) {
+    const double e = __ldg(err + j);
+    const uint8_t code = probe_code(s_s, ts.nan_cnt, __ldg(flag + j), e);
+#pragma unroll
+    for (int k = 0; k < kMaxProbes; ++k) {
+      const bool cand = code > ts.pos[k];
+      acc[k] += cand ? 0.0 : e;
+      c[k] += cand;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxProbes; ++k) {
+    double a = acc[k];
+    int cc = c[k];
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    }
+    if (lane == 0) {
+      s_acc[w][k] = a;
+      s_c[w][k] = cc;
+    }
+  }
+  __syncthreads();
+  if (tid < kMaxProbes) {
+    double a = 0.0;
+    long long cc = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      a += s_acc[q][tid];
+      cc += s_c[q][tid];
+    }
+    part[tid * gridDim.x + blockIdx.x] = a;
+    cnt[tid * gridDim.x + blockIdx.x] = cc;
+  }
+}
+
+// The accepted threshold's exact sums (reduce.cpp:31-64 under the final flags
+// flag && !(err < t)): per 2048-block, warp 0 folds the estimates and warp 1
+// the errors of the non-candidates, strictly in order.  Each warp loads
+// 64-element chunks coalesced (the next chunk in flight while the current one
+// is folded) and broadcasts them with shuffles, so the chain runs at the DADD
+// latency instead of waiting on memory.  part[q * nblk + b]: q = 0 est, 1 err;
+// cnt[b] = candidates.
+__global__ void __launch_bounds__(64)
+    k_fold_threshold(int64_t m, int64_t nblk, const double* __restrict__ est,
+                     const double* __restrict__ err, const uint8_t* __restrict__ flag, double t,
+                     double* part, int64_t* cnt) {
+  const int64_t b = blockIdx.x;
+  const int64_t lo = b * kBlock;
+  const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const double* x = q ? err : est;
+  auto load = [&](int c, double& v0, double& v1, int& k0, int& k1) {
+    const int i0 = c * 64 + lane, i1 = i0 + 32;
+    double x0 = 0.0, x1 = 0.0, e0 = 0.0, e1 = 0.0;
+    uint8_t f0 = 0, f1 = 0;
+    if (i0 < n) {
+      f0 = __ldg(flag + lo + i0);
+      e0 = __ldg(err + lo + i0);
+      x0 = q ? e0 : __ldg(x + lo + i0);
+    }
+    if (i1 < n) {
+      f1 = __ldg(flag + lo + i1);
+      e1 = __ldg(err + lo + i1);
+      x1 = q ? e1 : __ldg(x + lo + i1);
+    }
+    k0 = f0 && !(e0 < t);  // candidate: stays active (classify.cpp:63-66)
+    k1 = f1 && !(e1 < t);
+    v0 = k0 ? 0.0 : x0;    // the masked fold skips it; +0.0 is the same
+    v1 = k1 ? 0.0 : x1;
+  };
+  const int nch = (n + 63) / 64;
+  double s = 0.0;
+  long long kept = 0;
+  double v0, v1;
+  int k0, k1;
+  load(0, v0, v1, k0, k1);
+  for (int c = 0; c < nch; ++c) {
+    double w0 = 0.0, w1 = 0.0;
+    int j0 = 0, j1 = 0;
+    if (c + 1 < nch) load(c + 1, w0, w1, j0, j1);  // next chunk in flight
+    kept += __popc(__ballot_sync(0xffffffffu, k0)) + __popc(__ballot_sync(0xffffffffu, k1));
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s = P_ADD(s, __shfl_sync(0xffffffffu, v0, k));
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s = P_ADD(s, __shfl_sync(0xffffffffu, v1, k));
+    v0 = w0, v1 = w1, k0 = j0, k1 = j1;
+  }
+  if (lane == 0) {
+    part[q * nblk + b] = s;
+    if (q == 0) cnt[b] = kept;
+  }
+}
+
+// Totals over the G CTAs of k_probe_fast into mapped host memory (err_sum =
+// the fast sums, count exact), then publish `seq`.
+__global__ void __launch_bounds__(512)
+    k_probe_fast_total(int G, const double* part, const int64_t* cnt, ProbeScalars* out,
+                       unsigned* ready, unsigned seq) {
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;  // 16 warps: one per node
+  double a = 0.0;
+  long long n = 0;
+  if (k < kMaxProbes) {
+#pragma unroll 8
+    for (int g = lane; g < G; g += 32) {  // independent loads, issued ahead
+      a += part[k * G + g];
+      n += cnt[k * G + g];
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  if (k < kMaxProbes && lane == 0) {
+    out->err_sum[k] = a;
+    out->est_sum[k] = 0.0;
+    out->count[k] = n;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ready) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(ready) = seq;
   }
 }
 
@@ -937,11 +1096,11 @@ void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap,
 }
 
 void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
-                      const uint8_t* flag, double* part, int64_t* cnt) {
+                      const uint8_t* flag, double* part, int64_t* cnt, int use_t, double t) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   k_fold_eval<<<static_cast<unsigned>(nblk), kFoldThreads, 0, st>>>(m, nblk, est, err, flag,
-                                                                     part, cnt);
+                                                                     part, cnt, use_t, t);
 }
 
 
@@ -1008,6 +1167,28 @@ void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const do
   k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
                                                                         flag, part, cnt);
   finalize_multi(st, nblk, ts.T, part, cnt, scratch, out, ready, seq, done);
+}
+
+int probe_fast_grid(int64_t m) {
+  const int64_t want = (m + 8 * kPfThreads - 1) / (8 * kPfThreads);  // >= 8 regions per thread
+  const int64_t cap = 148 * 8;
+  return static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+void launch_probe_fast(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* err,
+                       const uint8_t* flag, double* part, int64_t* cnt, ProbeScalars* out,
+                       unsigned* ready, unsigned seq) {
+  const int G = probe_fast_grid(m);
+  if (m > 0) k_probe_fast<<<G, kPfThreads, 0, st>>>(m, ts, err, flag, part, cnt);
+  k_probe_fast_total<<<1, 512, 0, st>>>(m > 0 ? G : 0, part, cnt, out, ready, seq);
+}
+
+void launch_fold_threshold(cudaStream_t st, int64_t m, const double* est, const double* err,
+                           const uint8_t* flag, double t, double* part, int64_t* cnt) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk > 0)
+    k_fold_threshold<<<static_cast<unsigned>(nblk), 64, 0, st>>>(m, nblk, est, err, flag, t, part,
+                                                                 cnt);
 }
 
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets) {

@@ -66,8 +66,10 @@ void launch_uniform_split(cudaStream_t st, int n, int d, int64_t m, int64_t cap,
 
 // Post-evaluation block folds: q0 = sum est, q1 = sum err,
 // q2 = sum est[flag==0] (+ count flag==1), q3 = sum err[flag==0].
+// use_t: under the final flags of threshold t (flag && !(err < t)).
 void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const double* err,
-                      const uint8_t* flag, double* part, int64_t* cnt);
+                      const uint8_t* flag, double* part, int64_t* cnt, int use_t = 0,
+                      double t = 0.0);
 
 // Candidate flags of an accepted threshold (classify.cpp:63-66), batch API.
 void launch_candidates(cudaStream_t st, int64_t m, double t, const uint8_t* flag,
@@ -95,6 +97,18 @@ void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const do
                         double* scratch, ProbeScalars* out, unsigned* ready = nullptr,
                         unsigned seq = 0, int* done = nullptr);
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets);
+
+// Fast probe pass (exact counts, fast sums of the discarded error per node)
+// into mapped `out`, published with `seq`.  part / cnt: kMaxProbes x
+// probe_fast_grid(m) scratch.
+int probe_fast_grid(int64_t m);
+// Exact block folds of est (q = 0) and err (q = 1) over the non-candidates
+// of threshold t, and per-block candidate counts: part[q * nblk + b], cnt[b].
+void launch_fold_threshold(cudaStream_t st, int64_t m, const double* est, const double* err,
+                           const uint8_t* flag, double t, double* part, int64_t* cnt);
+void launch_probe_fast(cudaStream_t st, int64_t m, const ProbeSet& ts, const double* err,
+                       const uint8_t* flag, double* part, int64_t* cnt, ProbeScalars* out,
+                       unsigned* ready, unsigned seq);
 
 // min_max over err (reduce.cpp:74-82).  out[0] = min, out[1] = max, as doubles.
 void launch_minmax(cudaStream_t st, int64_t m, const double* x, unsigned long long* keys,

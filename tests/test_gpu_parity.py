@@ -538,3 +538,40 @@ def test_batch_functions_on_empty_and_tiny_inputs(pg, gpu, ref):
                                          float(err.sum()), m, 1e-3)
             assert got.success == exp["success"] and got.attempts == exp["attempts"]
             assert np.array_equal(got.flags, exp["flags"])
+
+
+def test_streamed_threshold_search_equals_exact_folds(pg, gpu, tmp_path):
+    """PAGANI_PROBE_STREAM=1 decides the threshold search from streamed passes
+    (exact counts, fast sums with a rounding bound) and folds only the accepted
+    threshold exactly; the default runs every pass with the strict folds.
+    Both must give the same trace bit for bit."""
+    import json
+    import subprocess
+    import sys
+    cases = [(1, 8, 1e-3, False, 30), (6, 8, 1e-4, True, 60), (2, 8, 1e-3, True, 40)]
+    code = ("import json,sys; sys.path.insert(0, %r); import paper_2104_06494_b200 as pg\n"
+            "out=[]\n"
+            "for f,n,tau,relf,itm in %r:\n"
+            "    r=pg.integrate(pg.Integrand(f), pg.Bounds.unit_cube(n),"
+            " pg.Config(tau_rel=tau, rel_filtering_enabled=relf, it_max=itm), trace=True)\n"
+            "    out.append([r.estimate.hex(), r.errorest.hex(), r.iterations, r.regions_generated,"
+            " [[row[k].hex() if isinstance(row[k], float) else row[k] for k in sorted(row)]"
+            " for row in r.trace], r.probe_fallbacks, len(r.threshold_events)])\n"
+            "print(json.dumps(out))\n") % (str(pg.__path__[0]).rsplit("/", 1)[0], cases)
+    env = dict(__import__("os").environ, PAGANI_PROBE_STREAM="1")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr
+    streamed = json.loads(p.stdout.strip().splitlines()[-1])
+    fallbacks = 0
+    for (f, n, tau, relf, itm), got in zip(cases, streamed):
+        r = pg.integrate(pg.Integrand(f), pg.Bounds.unit_cube(n),
+                         pg.Config(tau_rel=tau, rel_filtering_enabled=relf, it_max=itm),
+                         trace=True)
+        want = [r.estimate.hex(), r.errorest.hex(), r.iterations, r.regions_generated,
+                [[row[k].hex() if isinstance(row[k], float) else row[k] for k in sorted(row)]
+                 for row in r.trace]]
+        assert got[:5] == want, (f, n, tau)
+        assert got[6] > 0  # threshold searches happened
+        fallbacks += got[5]
+    assert fallbacks <= 2  # the streamed passes decide (nearly) always

@@ -9,8 +9,15 @@ import json
 import sys
 
 
+def _open(path):
+    if path.endswith(".gz"):
+        import gzip
+        return gzip.open(path, "rt")
+    return open(path)
+
+
 def _table(path):
-    rows = list(csv.reader(open(path)))
+    rows = list(csv.reader(_open(path)))
     for i, r in enumerate(rows):
         if "Kernel Name" in r or "ID" in r[:1]:
             return rows[i], rows[i + 1:]
