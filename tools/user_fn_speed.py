@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2104_06494_b200 as pg  # noqa: E402
 
-lib = C.CDLL(os.path.join(ROOT, "tests", "ext", "libuser_integrands.so"))
+lib = C.CDLL(os.environ.get("USER_LIB") or os.path.join(ROOT, "tests", "ext", "libuser_integrands.so"))
 D = C.POINTER(C.c_double)
 lib.user_integrate.argtypes = [C.c_int, D, C.c_int, C.c_double, C.c_int, C.c_int, D, D, D,
                                C.POINTER(C.c_int64)]
