@@ -5,6 +5,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -1481,6 +1482,151 @@ __global__ void __launch_bounds__(kBulkThreads, 3)
   }
 }
 
+// Persistent form of k_split_bulk (N >= 2): one CTA per resident slot, each
+// walking the blocks b = blockIdx.x, + gridDim.x, ... that have kept
+// regions.  The CTA's geometry rows form one stream g = 0, 1, 2, ... (row a
+// of its i-th block is g = i N + a), staged through the same 2-slot ring
+// (slot g & 1, mbarrier phase (g >> 1) & 1); a freed slot is refilled with row
+// g + 2 -- for the last two rows of a block that is the next block's first
+// two rows, so the next block's loads are in flight while this block is
+// finished and the next block's flags are scanned, and there is no wave tail.
+template <int N>
+__global__ void __launch_bounds__(kBulkThreads, 3)
+    k_split_bulk_p(int64_t m, int64_t nblk, int64_t cap_src, int64_t cap_stage,
+                   const uint8_t* __restrict__ flag, int use_t, double t,
+                   const int64_t* __restrict__ offsets, int64_t kept_end,
+                   const double* __restrict__ est, const double* __restrict__ err,
+                   const uint8_t* __restrict__ axis, const double* __restrict__ low,
+                   const double* __restrict__ len, double* __restrict__ dlow0,
+                   double* __restrict__ dlen0, double* __restrict__ dpest0, int64_t kbase,
+                   SplitWindow win) {
+  static_assert(N >= 2, "the persistent split streams two rows ahead within a block pair");
+  constexpr int W = kBulkThreads / 32;
+  extern __shared__ __align__(128) double sbuf[];  // [slot][low | len][kBlock]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_cnt[kBulkPer][W];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  auto kfirst = [&](int64_t b) { return offsets[b]; };
+  auto knext = [&](int64_t b) { return b + 1 < nblk ? offsets[b + 1] : kept_end; };
+  auto next_block = [&](int64_t b) {  // the CTA's next block with kept regions
+    while (b < nblk && knext(b) == kfirst(b)) b += gridDim.x;
+    return b;
+  };
+  auto row_bytes = [&](int64_t b) {
+    const int64_t c = m - b * kBlock < kBlock ? m - b * kBlock : kBlock;
+    return static_cast<uint32_t>(((c + 1) & ~int64_t{1}) * sizeof(double));
+  };
+  auto issue = [&](int64_t b, int a, int slot) {  // one thread: rows low[a], len[a] of block b
+    const uint32_t rb = row_bytes(b);
+    mbar_expect_tx(&bar[slot], 2 * rb);
+    bulk_g2s(sbuf + (2 * slot) * kBlock, low + a * cap_src + b * kBlock, rb, &bar[slot]);
+    bulk_g2s(sbuf + (2 * slot + 1) * kBlock, len + a * cap_src + b * kBlock, rb, &bar[slot]);
+  };
+  int64_t b = next_block(blockIdx.x);
+  if (b >= nblk) return;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    issue(b, 0, 0);
+    issue(b, 1, 1);
+  }
+  uint32_t g = 0;  // global row counter of this CTA
+  while (b < nblk) {
+    const int64_t bn = next_block(b + gridDim.x);
+    const int64_t base = b * kBlock;
+    const int cnt = static_cast<int>(m - base < kBlock ? m - base : kBlock);
+    bool keep[kBulkPer];
+    unsigned before[kBulkPer];
+#pragma unroll
+    for (int r = 0; r < kBulkPer; ++r) {
+      const int i = r * kBulkThreads + tid;
+      const int64_t j = base + i;
+      const uint8_t fl = i < cnt ? (flag ? __ldg(flag + j) : uint8_t{1}) : uint8_t{0};
+      const double ev = (use_t && i < cnt) ? __ldg(err + j) : 0.0;
+      keep[r] = fl != 0 && !(use_t && ev < t);  // classify.cpp:63-66
+      const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
+      before[r] = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) s_cnt[r][wid] = __popc(bal);
+    }
+    __syncthreads();
+    int64_t run = kfirst(b);
+    int64_t c0[kBulkPer];
+    bool inwin[kBulkPer];
+    uint32_t ax_pack[2] = {0u, 0u};
+#pragma unroll
+    for (int r = 0; r < kBulkPer; ++r) {
+      int wbase = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int c = s_cnt[r][w];
+        wbase += w < wid ? c : 0;
+        tot += c;
+      }
+      const int64_t k = run + wbase + before[r];
+      run += tot;
+      int64_t c = 2 * (k - kbase);
+      inwin[r] = win.low && c >= win.lo && c < win.hi;
+      if (inwin[r]) c += win.dst - win.lo;
+      c0[r] = c;
+      if (keep[r]) {
+        const int64_t j = base + r * kBulkThreads + tid;
+        const double e = __ldg(est + j);
+        double* dp = inwin[r] ? win.pest : dpest0;
+        *reinterpret_cast<double2*>(dp + c) = make_double2(e, e);
+        ax_pack[r >> 2] |= static_cast<uint32_t>(__ldg(axis + j)) << (8 * (r & 3));
+      }
+    }
+#pragma unroll 1
+    for (int a = 0; a < N; ++a, ++g) {
+      const int slot = static_cast<int>(g & 1u);
+      mbar_wait(&bar[slot], (g >> 1) & 1u);
+      const double* sl = sbuf + (2 * slot) * kBlock;
+      const double* sn = sbuf + (2 * slot + 1) * kBlock;
+#pragma unroll
+      for (int r = 0; r < kBulkPer; ++r) {
+        if (!keep[r]) continue;
+        const int i = r * kBulkThreads + tid;
+        const double lo = sl[i], ln = sn[i];
+        const int ax = static_cast<int>((ax_pack[r >> 2] >> (8 * (r & 3))) & 0xffu);
+        double2 cl, cn;
+        if (a == ax) {  // geometry.cpp:122-141
+          const double half = P_MUL(ln, 0.5);
+          cl = make_double2(lo, P_ADD(lo, half));
+          cn = make_double2(half, half);
+        } else {
+          cl = make_double2(lo, lo);
+          cn = make_double2(ln, ln);
+        }
+        double* dl = inwin[r] ? win.low : dlow0;
+        double* dn = inwin[r] ? win.len : dlen0;
+        const int64_t capd = inwin[r] ? win.cap : cap_stage;
+        *reinterpret_cast<double2*>(dl + a * capd + c0[r]) = cl;
+        *reinterpret_cast<double2*>(dn + a * capd + c0[r]) = cn;
+      }
+      __syncthreads();  // every thread is done with this slot (and with s_cnt)
+      if (tid == 0) {   // refill it with the stream's row g + 2
+        if (a + 2 < N)
+          issue(b, a + 2, slot);
+        else if (bn < nblk)
+          issue(bn, a + 2 - N, slot);
+      }
+    }
+    b = bn;
+  }
+}
+
+// PAGANI_SPLIT_PERSISTENT=1 selects the persistent k_split_bulk_p (A/B:
+// measured slower on B200 -- 112.4 vs 107.0 ms per bench step -- so the
+// one-CTA-per-block form is the default).
+static bool split_persistent() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_SPLIT_PERSISTENT");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t cap_dst,
                   const uint8_t* flag, int use_t, double t, const int64_t* offsets,
                   const double* est,
@@ -1490,6 +1636,31 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   const unsigned g = static_cast<unsigned>(nblk);
+  if (bulk && offsets && kept_end >= 0 && !dperr && n >= 2 && n <= 16 && split_persistent()) {
+    static int sms = [] {
+      int d = 0, v = 148;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+      return v;
+    }();
+    const int64_t slots = static_cast<int64_t>(sms) * 3;
+    const unsigned gp = static_cast<unsigned>(nblk < slots ? nblk : slots);
+    switch (n) {
+#define PGN_BULKP_CASE(NN)                                                                     \
+  case NN:                                                                                     \
+    opt_in_smem(reinterpret_cast<const void*>(&k_split_bulk_p<NN>));                          \
+    k_split_bulk_p<NN><<<gp, kBulkThreads, kBulkSmem, st>>>(                                   \
+        m, nblk, cap_src, cap_dst, flag, use_t, t, offsets, kept_end, est, err, axis, low, len, \
+        dlow, dlen, dpest, kbase, win);                                                        \
+    return;
+      PGN_BULKP_CASE(2) PGN_BULKP_CASE(3) PGN_BULKP_CASE(4) PGN_BULKP_CASE(5)
+      PGN_BULKP_CASE(6) PGN_BULKP_CASE(7) PGN_BULKP_CASE(8) PGN_BULKP_CASE(9) PGN_BULKP_CASE(10)
+      PGN_BULKP_CASE(11) PGN_BULKP_CASE(12) PGN_BULKP_CASE(13) PGN_BULKP_CASE(14)
+      PGN_BULKP_CASE(15) PGN_BULKP_CASE(16)
+#undef PGN_BULKP_CASE
+      default: break;
+    }
+  }
   if (bulk && offsets && kept_end >= 0 && !dperr && n >= 1 && n <= 16) {
     switch (n) {
 #define PGN_BULK_CASE(NN)                                                                      \
