@@ -12,6 +12,7 @@
 
 #include <array>
 #include <cmath>
+#include <cstring>
 #include <stdexcept>
 #include <vector>
 
@@ -268,6 +269,11 @@ RuleOrbits build_rule_orbits(int n) {
   r.gen[1] = static_cast<double>(kL3);
   r.gen[2] = static_cast<double>(kL4);
   r.gen[3] = static_cast<double>(kL5);
+  // The degree-5 rule has no corner orbit, so the first null rule's corner
+  // weight is w7's exactly (u1 = w7 - 0).  k_evaluate_sep relies on it: one
+  // product w * f serves the corner points' S[0] and S[1] sums.
+  if (n >= 2 && std::memcmp(&r.w[0][kCorners], &r.w[1][kCorners], sizeof(double)) != 0)
+    throw std::logic_error("build_rule: corner weights of the rule and its first null rule differ");
   return r;
 }
 

@@ -52,6 +52,15 @@ def test_rule_weights_bit_identical_to_reference(pg, ref):
         assert np.array_equal(bits(ws), bits(rws)), n
 
 
+def test_corner_orbit_weights_of_rule_and_first_null_rule_are_equal(pg):
+    """The degree-5 rule has no corner orbit, so the first null rule's corner
+    weight equals the degree-7 rule's bit for bit (n >= 2); k_evaluate shares
+    the product w * f between those two sums on the corner points."""
+    for n in range(2, 17):
+        w, _, _, _ = pg.build_rule(n)
+        assert bits(np.array([w[0, 4]]))[0] == bits(np.array([w[1, 4]]))[0], n
+
+
 def test_rule_point_counts_and_weight_sums(pg):
     """test_rule.cpp:58-80."""
     assert pg.rule_point_count(1) == 7
