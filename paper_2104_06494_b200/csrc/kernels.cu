@@ -396,61 +396,67 @@ __global__ void __launch_bounds__(kPfThreads)
 }
 
 // The accepted threshold's exact sums (reduce.cpp:31-64 under the final flags
-// flag && !(err < t)): per 2048-block, warp 0 folds the estimates and warp 1
-// the errors of the non-candidates, strictly in order.  Each warp loads
-// 64-element chunks coalesced (the next chunk in flight while the current one
-// is folded) and broadcasts them with shuffles, so the chain runs at the DADD
-// latency instead of waiting on memory.  part[q * nblk + b]: q = 0 est, 1 err;
-// cnt[b] = candidates.
-__global__ void __launch_bounds__(64)
+// flag && !(err < t)): per 2048-block the CTA stages the masked estimates and
+// errors (0.0 for candidates: adding +0.0 is the reference's skip) into
+// shared memory with all its threads, then one thread per quantity folds the
+// block strictly in order from shared memory, eight loads ahead of the DADD
+// chain.  part[q * nblk + b]: q = 0 est, 1 err; cnt[b] = candidates.
+constexpr int kFtThreads = 256;
+__global__ void __launch_bounds__(kFtThreads)
     k_fold_threshold(int64_t m, int64_t nblk, const double* __restrict__ est,
                      const double* __restrict__ err, const uint8_t* __restrict__ flag, double t,
                      double* part, int64_t* cnt) {
+  __shared__ __align__(16) double s_v[2][kBlock];
   const int64_t b = blockIdx.x;
   const int64_t lo = b * kBlock;
   const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
-  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const double* x = q ? err : est;
-  auto load = [&](int c, double& v0, double& v1, int& k0, int& k1) {
-    const int i0 = c * 64 + lane, i1 = i0 + 32;
-    double x0 = 0.0, x1 = 0.0, e0 = 0.0, e1 = 0.0;
-    uint8_t f0 = 0, f1 = 0;
-    if (i0 < n) {
-      f0 = __ldg(flag + lo + i0);
-      e0 = __ldg(err + lo + i0);
-      x0 = q ? e0 : __ldg(x + lo + i0);
+  __shared__ int s_kept[kFtThreads / 32];
+  int kept = 0;
+#pragma unroll
+  for (int r = 0; r < kBlock / kFtThreads; ++r) {  // all loads issued before any use
+    const int i = r * kFtThreads + threadIdx.x;
+    double e = 0.0, x = 0.0;
+    bool k = false;
+    if (i < n) {
+      const uint8_t f = __ldg(flag + lo + i);
+      e = __ldg(err + lo + i);
+      x = __ldg(est + lo + i);
+      k = f && !(e < t);  // candidate: stays active (classify.cpp:63-66)
     }
-    if (i1 < n) {
-      f1 = __ldg(flag + lo + i1);
-      e1 = __ldg(err + lo + i1);
-      x1 = q ? e1 : __ldg(x + lo + i1);
-    }
-    k0 = f0 && !(e0 < t);  // candidate: stays active (classify.cpp:63-66)
-    k1 = f1 && !(e1 < t);
-    v0 = k0 ? 0.0 : x0;    // the masked fold skips it; +0.0 is the same
-    v1 = k1 ? 0.0 : x1;
-  };
-  const int nch = (n + 63) / 64;
+    s_v[0][i] = k ? 0.0 : x;
+    s_v[1][i] = k ? 0.0 : e;
+    kept += k;
+  }
+  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+  if ((threadIdx.x & 31) == 0) s_kept[threadIdx.x >> 5] = kept;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    kept = 0;
+#pragma unroll
+    for (int w = 0; w < kFtThreads / 32; ++w) kept += s_kept[w];
+  }
+  if (threadIdx.x != 0 && threadIdx.x != 32) return;
+  const int q = threadIdx.x >> 5;
+  const double* v = s_v[q];
   double s = 0.0;
-  long long kept = 0;
-  double v0, v1;
-  int k0, k1;
-  load(0, v0, v1, k0, k1);
-  for (int c = 0; c < nch; ++c) {
-    double w0 = 0.0, w1 = 0.0;
-    int j0 = 0, j1 = 0;
-    if (c + 1 < nch) load(c + 1, w0, w1, j0, j1);  // next chunk in flight
-    kept += __popc(__ballot_sync(0xffffffffu, k0)) + __popc(__ballot_sync(0xffffffffu, k1));
-#pragma unroll
-    for (int k = 0; k < 32; ++k) s = P_ADD(s, __shfl_sync(0xffffffffu, v0, k));
-#pragma unroll
-    for (int k = 0; k < 32; ++k) s = P_ADD(s, __shfl_sync(0xffffffffu, v1, k));
-    v0 = w0, v1 = w1, k0 = j0, k1 = j1;
+  const int n8 = n & ~7;
+  for (int i = 0; i < n8; i += 8) {
+    const double2 a = *reinterpret_cast<const double2*>(v + i);
+    const double2 c = *reinterpret_cast<const double2*>(v + i + 2);
+    const double2 d = *reinterpret_cast<const double2*>(v + i + 4);
+    const double2 f = *reinterpret_cast<const double2*>(v + i + 6);
+    s = P_ADD(s, a.x);
+    s = P_ADD(s, a.y);
+    s = P_ADD(s, c.x);
+    s = P_ADD(s, c.y);
+    s = P_ADD(s, d.x);
+    s = P_ADD(s, d.y);
+    s = P_ADD(s, f.x);
+    s = P_ADD(s, f.y);
   }
-  if (lane == 0) {
-    part[q * nblk + b] = s;
-    if (q == 0) cnt[b] = kept;
-  }
+  for (int i = n8; i < n; ++i) s = P_ADD(s, v[i]);
+  part[q * nblk + b] = s;
+  if (q == 0) cnt[b] = kept;
 }
 
 // Totals over the G CTAs of k_probe_fast into mapped host memory (err_sum =
@@ -1188,8 +1194,8 @@ void launch_fold_threshold(cudaStream_t st, int64_t m, const double* est, const 
                            const uint8_t* flag, double t, double* part, int64_t* cnt) {
   const int64_t nblk = nblocks_of(m);
   if (nblk > 0)
-    k_fold_threshold<<<static_cast<unsigned>(nblk), 64, 0, st>>>(m, nblk, est, err, flag, t, part,
-                                                                 cnt);
+    k_fold_threshold<<<static_cast<unsigned>(nblk), kFtThreads, 0, st>>>(m, nblk, est, err, flag,
+                                                                         t, part, cnt);
 }
 
 void launch_scan_counts(cudaStream_t st, int64_t nblk, const int64_t* cnt, int64_t* offsets) {
