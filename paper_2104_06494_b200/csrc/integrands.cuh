@@ -145,6 +145,9 @@ struct F3 {  // (1 + sum (i+1) x_i)^-(n+1)       integrands.cpp:39-43
   PGN_HD static bool cut(int, double) { return false; }
 };
 
+#ifndef PGN_F4_UNDERFLOW_SKIP
+#define PGN_F4_UNDERFLOW_SKIP 0  // A/B knob
+#endif
 struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
   static constexpr bool kSeparable = true, kCut = false;
   static constexpr bool kCornerRegs = true;  // evaluate.cuh corner_regs
@@ -159,7 +162,17 @@ struct F4 {  // exp(-625 sum (x-1/2)^2)          integrands.cpp:45-52
     return tab_exp(P_MUL(-625.0, s), T);
   }
   PGN_HD static void fin2(double s0, double s1, int, const MathTables& T, double& f0, double& f1) {
-    tab_exp2(P_MUL(-625.0, s0), P_MUL(-625.0, s1), T, f0, f1);
+    const double x0 = P_MUL(-625.0, s0), x1 = P_MUL(-625.0, s1);
+#if PGN_F4_UNDERFLOW_SKIP
+    // both below -746: exp is +0 on every path of e_exp.c (tested against
+    // libm), and far from the peak in 8D/10D most corner pairs are
+    if (x0 < -746.0 && x1 < -746.0) {
+      f0 = 0.0;
+      f1 = 0.0;
+      return;
+    }
+#endif
+    tab_exp2(x0, x1, T, f0, f1);
   }
   PGN_HD static bool cut(int, double) { return false; }
 };
