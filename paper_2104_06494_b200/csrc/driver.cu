@@ -1,13 +1,19 @@
-// The PAGANI iteration (Alg. 2) on one B200: host C++ makes every scalar
-// decision exactly as /root/reference/proj/src/driver.cpp:83-215 does; the
-// region list never leaves HBM.  Per iteration:
+// The PAGANI iteration (Alg. 2) on one B200 (or R sharded GPUs): host C++
+// makes every scalar decision exactly as /root/reference/proj/src/driver.cpp:83-215
+// does; the region list never leaves HBM.  Per iteration:
 //
-//   k_evaluate  (rule + two-level refine + rel-err classify, fused)
-//   k_fold_eval (serial 2048-block partials of est, err, finished est/err,
-//                active counts)  ->  k_finalize (pairwise trees, offsets)
-//   -- one 48-byte D2H of the scalars, host decisions --
-//   [threshold search: k_minmax, then per probe k_probe -> k_finalize -> D2H]
-//   k_split     (fused filter + bisect into the other buffer)
+//   k_evaluate  (rule + integrand + 4th differences + two-level refine +
+//                rel-err classify, fused; its tail folds each 2048-block
+//                serially: partials of est, err, finished est/err, active
+//                counts, error min/max)
+//   k_finalize  (pairwise trees, kept offsets) -> 64 bytes into mapped host
+//                memory, a published sequence number (zero-copy hand-off)
+//   -- host decisions --
+//   [threshold search: per pass k_probe_multi (15 speculative thresholds) ->
+//    k_finalize_multi -> 360 bytes zero-copy; the host replays the decisions]
+//   k_split_bulk (fused filter + bisect into the other buffer, TMA-staged rows)
+//   [sharded: allgathered block records before the trees, the boundary
+//    exchange after the split -- DESIGN.md 7]
 //
 // Host arithmetic is compiled with -ffp-contract=off and uses the same
 // expression order as the reference, so v, e, v_f, e_f, budgets and
