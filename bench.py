@@ -325,7 +325,9 @@ def run_ours(args, rank, world, local_rank):
     # counted by the driver per launch) / their CUDA-event time.
     hbm_peak, hbm_src = measured_hbm_peak()
     hbm = {}
-    for k, label in (("split", "k_split (filter + bisect)"),
+    split_label = ("k_split (filter + bisect)" if os.environ.get("PAGANI_DEFER_BISECT") == "0"
+                   else "k_link (filter; the bisection is deferred into k_evaluate, DESIGN.md 4)")
+    for k, label in (("split", split_label),
                      ("probe", "k_probe_multi + trees (threshold classify)")):
         ms = sum(r.kernel_ms[k] for st in steps for _, _, r in st)
         by = sum(r.kernel_bytes[k] for st in steps for _, _, r in st)

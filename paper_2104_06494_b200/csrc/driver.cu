@@ -54,6 +54,7 @@ void Workspace::ensure(int n_, int64_t cap_) {
     len[b].alloc(static_cast<size_t>(nn) * nc);
   }
   pest.alloc(nc);
+  link.alloc(nc / 2 + 1);
   est.alloc(nc);
   err.alloc(nc);
   axis.alloc(nc);
@@ -253,6 +254,16 @@ bool probe_stream() {
   static const bool on = [] {
     const char* e = std::getenv("PAGANI_PROBE_STREAM");
     return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Deferred bisection on one GPU (k_link + children derived in k_evaluate,
+// DESIGN.md 4); PAGANI_DEFER_BISECT=0 selects the explicit split kernel.
+bool defer_bisect() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_DEFER_BISECT");
+    return !e || std::atoi(e) != 0;
   }();
   return on;
 }
@@ -754,11 +765,17 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   };
 
   bool done = false;
+  bool linked = false;  // this batch's geometry still lives in its parents' rows (k_link)
   for (int it = 1; it <= cfg.it_max && !done; ++it) {
     // ---- evaluate (+ refine + classify + block folds) -------------------------
     ep.m = m;
     ep.low = ws.low[cur].p;
     ep.len = ws.len[cur].p;
+    // deferred bisection: the children are derived from the parent rows in
+    // the other buffer and written to this one by k_evaluate
+    ep.link = linked ? ws.link.p : nullptr;
+    ep.plow = linked ? ws.low[cur ^ 1].p : nullptr;
+    ep.plen = linked ? ws.len[cur ^ 1].p : nullptr;
     ep.refine = (it > 1 && cfg.refiner == PAGANI_REFINER_TWO_LEVEL) ? 1 : 0;
     const size_t k0 = kt.mark();
     const int64_t nblk = nblocks_of(m);
@@ -777,7 +794,11 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     kt.span(PAGANI_K_EVALUATE, k0, k1);
     out->kernel_launches[PAGANI_K_EVALUATE] += m > 0;
     // reads low/len (16n) [+ pest 8], writes est, err (16) + flag, axis (2)
-    out->kernel_bytes[PAGANI_K_EVALUATE] += static_cast<double>(m) * (16.0 * n + (ep.refine ? 8 : 0) + 18);
+    // (+ deferred bisection: the link (8 per sibling pair) and the child's
+    // row written back, 16n; the parent rows are counted as the read)
+    out->kernel_bytes[PAGANI_K_EVALUATE] +=
+        static_cast<double>(m) * (16.0 * n + (ep.refine ? 8 : 0) + 18) +
+        (linked ? static_cast<double>(m) * (16.0 * n + 4.0) : 0.0);
     out->eval_count += M * rule.point_count;
     out->region_evals += m;
 
@@ -968,8 +989,13 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
     // ---- fused filter + bisect (+ the exchange that re-balances the shards) ---
     const size_t k4 = kt.mark();
-    {  // flag (+ err under a threshold) for every region; est, axis, low, len of
-       // each kept one; two children (low, len, parent est) per kept region.
+    const bool defer = !sh && defer_bisect() && eval_k.fn_link != nullptr;
+    if (defer) {
+      // flag, axis, est (+ err under a threshold) per region; link + pest per kept
+      out->kernel_bytes[PAGANI_K_SPLIT] +=
+          static_cast<double>(m) * (use_t ? 18.0 : 10.0) + static_cast<double>(kept) * 16.0;
+    } else {  // flag (+ err under a threshold) for every region; est, axis, low, len of
+              // each kept one; two children (low, len, parent est) per kept region.
       const double kl = sh ? static_cast<double>(kb[rank + 1] - kb[rank]) : static_cast<double>(kept);
       out->kernel_bytes[PAGANI_K_SPLIT] += static_cast<double>(m) * (use_t ? 9.0 : 1.0) +
                                            kl * (16.0 * n + 9.0) + 2.0 * kl * (16.0 * n + 8.0);
@@ -977,7 +1003,13 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     // k_split_bulk (TMA-staged rows; measured 3-4% faster than k_split_n per
     // bench step); PAGANI_SPLIT_BULK=0 selects k_split_n
     const bool bulk = split_bulk_mode() != 0;
-    if (!sh) {
+    if (defer) {
+      launch_link(st, m, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p, ws.err.p,
+                  ws.axis.p, ws.link.p, ws.pest.p);
+      PGN_CK(cudaGetLastError());
+      out->kernel_launches[PAGANI_K_SPLIT]++;
+      m = 2 * kept;
+    } else if (!sh) {
       launch_split(st, n, m, cap, cap, ws.flag.p, use_t ? 1 : 0, t_accepted, offsets, ws.est.p,
                    ws.err.p, ws.axis.p, ws.low[cur].p, ws.len[cur].p, ws.low[cur ^ 1].p,
                    ws.len[cur ^ 1].p, ws.pest.p, nullptr, 0, SplitWindow{}, bulk, kept);
@@ -1034,6 +1066,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       m = sh->local();
     }
     if (!sh) kt.span(PAGANI_K_SPLIT, k4, kt.mark());
+    linked = defer;
     cur ^= 1;
     M = 2 * kept;
     out->regions_generated += M;

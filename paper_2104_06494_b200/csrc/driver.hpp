@@ -62,6 +62,7 @@ struct Workspace {
   int64_t nblk_cap = 0;
   DevBuf<double> low[2], len[2];
   DevBuf<double> pest, est, err;
+  DevBuf<uint64_t> link;               // deferred bisection: kept parent rows (k_link)
   DevBuf<uint8_t> axis, flag, flag2;
   DevBuf<double> part_eval, part_probe, scratch;
   DevBuf<int64_t> cnt_eval, cnt_probe, off_eval, off_probe;

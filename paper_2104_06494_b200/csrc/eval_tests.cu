@@ -22,9 +22,30 @@ EvalLaunch lookup_eval_f5(int, int);
 EvalLaunch lookup_eval_f6(int, int);
 EvalLaunch lookup_eval_f7(int, int);
 EvalLaunch lookup_eval_f8(int, int);
+EvalKernel lookup_eval_link_f1(int);
+EvalKernel lookup_eval_link_f2(int);
+EvalKernel lookup_eval_link_f3(int);
+EvalKernel lookup_eval_link_f4(int);
+EvalKernel lookup_eval_link_f5(int);
+EvalKernel lookup_eval_link_f6(int);
+EvalKernel lookup_eval_link_f7(int);
+EvalKernel lookup_eval_link_f8(int);
 
 EvalLaunch lookup_evaluate(int fid, int n, int mode) {
   if (n < 1 || n > 16) return {};
+  // built-ins: the direct form + (parity mode) the deferred-bisection form
+  using Direct = EvalLaunch (*)(int, int);
+  using Linked = EvalKernel (*)(int);
+  static const Direct direct[8] = {lookup_eval_f1, lookup_eval_f2, lookup_eval_f3, lookup_eval_f4,
+                                   lookup_eval_f5, lookup_eval_f6, lookup_eval_f7, lookup_eval_f8};
+  static const Linked linked[8] = {lookup_eval_link_f1, lookup_eval_link_f2, lookup_eval_link_f3,
+                                   lookup_eval_link_f4, lookup_eval_link_f5, lookup_eval_link_f6,
+                                   lookup_eval_link_f7, lookup_eval_link_f8};
+  if (fid >= 1 && fid <= 8) {
+    EvalLaunch k = direct[fid - 1](n, mode);
+    if (mode == 0) k.fn_link = linked[fid - 1](n);
+    return k;
+  }
   switch (fid) {
     case 1: return lookup_eval_f1(n, mode);
     case 2: return lookup_eval_f2(n, mode);
@@ -54,18 +75,20 @@ void launch_evaluate(const EvalLaunch& k, cudaStream_t st, const EvalParams& ep)
                       cudaGetErrorString(static_cast<cudaError_t>(rc)));
     return;
   }
+  const EvalKernel fn = ep.link ? k.fn_link : k.fn;
+  if (!fn) throw std::logic_error("launch_evaluate: no deferred-bisection form of this kernel");
   static std::mutex mu;
   static std::set<std::pair<int, const void*>> configured;
   int dev = 0;
   cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> g(mu);
-    if (k.smem > 0 && configured.insert({dev, reinterpret_cast<const void*>(k.fn)}).second)
-      cudaFuncSetAttribute(reinterpret_cast<const void*>(k.fn),
+    if (k.smem > 0 && configured.insert({dev, reinterpret_cast<const void*>(fn)}).second)
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem));
   }
   const unsigned grid = static_cast<unsigned>((ep.m + kEvalThreads - 1) / kEvalThreads);
-  k.fn<<<grid, kEvalThreads, k.smem, st>>>(ep, device_exp_table(), device_sincos_table());
+  fn<<<grid, kEvalThreads, k.smem, st>>>(ep, device_exp_table(), device_sincos_table());
 }
 
 }  // namespace pgn

@@ -256,11 +256,20 @@ __device__ __forceinline__ void probe_stage_chunk(ProbeStage& S, const ProbeSet&
   }
 }
 
-// s += v unless (word & bit) (the skip of reduce.cpp:59-60; adding +0.0
-// instead is identical: s starts at +0.0 and never becomes -0.0 under RN).
-// The select happens on the loaded value, off the DADD dependency chain.
+// s += v unless (word & bit): the skip of reduce.cpp:59-60 as a predicated
+// DADD (LOP3 -> predicate, @!P DADD: two instructions per step; the former
+// select form, adding +0.0 for a skipped region, cost LOP3 + 2 FSEL + DADD).
+#ifndef PGN_PROBE_PRED
+#define PGN_PROBE_PRED 0  // measured slower on B200: ptxas if-converts it to DADD + 2 FSEL after the add, on the chain
+#endif
 __device__ __forceinline__ void add_unless(double& s, double v, uint32_t word, uint32_t bit) {
+#if PGN_PROBE_PRED
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.b32 p, %2, 0;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
+      : "+d"(s)
+      : "d"(v), "r"(word & bit));
+#else
   s = P_ADD(s, (word & bit) ? 0.0 : v);
+#endif
 }
 
 __global__ void __launch_bounds__(kProbeThreads)
@@ -1703,6 +1712,74 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                                            err, axis, low, len, dlow, dlen, dpest, dperr, kbase,
                                            win);
   }
+}
+
+// ---- k_link: the filter half of k_split, bisection deferred into k_evaluate --
+// Region j is kept when flag && !(use_t && err < t) (classify.cpp:63-66,
+// 111-126); the k-th kept region (k = offsets[block] + rank in the block, the
+// filter's order) becomes link[k] = j | axis << 56 and pest[k] = est[j], and
+// the next k_evaluate derives children 2k, 2k+1 from that row
+// (geometry.cpp:122-141, evaluate.cuh load_geometry).  No geometry moves
+// here: 10-18 B read per region, 16 B written per kept region, all coalesced.
+constexpr int kLinkThreads = 512;
+constexpr int kLinkPer = static_cast<int>(kBlock) / kLinkThreads;  // 4
+__global__ void __launch_bounds__(kLinkThreads)
+    k_link(int64_t m, const uint8_t* __restrict__ flag, int use_t, double t,
+           const int64_t* __restrict__ offsets, const double* __restrict__ est,
+           const double* __restrict__ err, const uint8_t* __restrict__ axis,
+           uint64_t* __restrict__ link, double* __restrict__ pest) {
+  constexpr int W = kLinkThreads / 32;
+  __shared__ int s_cnt[kLinkPer][W];
+  const int64_t b = blockIdx.x;
+  const int64_t base = b * kBlock;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint8_t fl[kLinkPer], ax[kLinkPer];
+  double ev[kLinkPer], xv[kLinkPer];
+#pragma unroll
+  for (int r = 0; r < kLinkPer; ++r) {  // every load issued before any use
+    const int64_t j = base + r * kLinkThreads + threadIdx.x;
+    const bool in = j < m;
+    fl[r] = in ? __ldg(flag + j) : uint8_t{0};
+    ax[r] = in ? __ldg(axis + j) : uint8_t{0};
+    xv[r] = in ? __ldg(est + j) : 0.0;
+    ev[r] = (use_t && in) ? __ldg(err + j) : 0.0;
+  }
+  bool keep[kLinkPer];
+  unsigned before[kLinkPer];
+#pragma unroll
+  for (int r = 0; r < kLinkPer; ++r) {
+    keep[r] = fl[r] != 0 && !(use_t && ev[r] < t);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
+    before[r] = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_cnt[r][wid] = __popc(bal);
+  }
+  __syncthreads();
+  int64_t run = offsets[b];
+#pragma unroll
+  for (int r = 0; r < kLinkPer; ++r) {
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int c = s_cnt[r][w];
+      wbase += w < wid ? c : 0;
+      total += c;
+    }
+    const int64_t k = run + wbase + before[r];
+    run += total;
+    if (!keep[r]) continue;
+    const int64_t j = base + r * kLinkThreads + threadIdx.x;
+    link[k] = static_cast<uint64_t>(j) | (static_cast<uint64_t>(ax[r]) << 56);
+    pest[k] = xv[r];
+  }
+}
+
+void launch_link(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, double t,
+                 const int64_t* offsets, const double* est, const double* err,
+                 const uint8_t* axis, uint64_t* link, double* pest) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  k_link<<<static_cast<unsigned>(nblk), kLinkThreads, 0, st>>>(m, flag, use_t, t, offsets, est,
+                                                               err, axis, link, pest);
 }
 
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,

@@ -55,6 +55,7 @@ struct EvalLaunch {
   bool fused_fold = false;  // kernel runs the 2048-block folds in its tail
   const pagani_device_fn* ext = nullptr;  // caller-compiled kernel (PAGANI_DEVICE_FN)
   int mode = 0;                           // for ext
+  EvalKernel fn_link = nullptr;  // deferred-bisection form (EvalParams.link), when it exists
   bool valid() const { return fn != nullptr || ext != nullptr; }
 };
 
@@ -136,6 +137,12 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
                   double* dlow, double* dlen, double* dpest, double* dperr, int64_t kbase = 0,
                   const SplitWindow& win = SplitWindow{}, bool bulk = false,
                   int64_t kept_end = -1);
+
+// Filter only, bisection deferred into the next k_evaluate (EvalParams.link):
+// link[k] = j | axis[j] << 56, pest[k] = est[j] for the k-th kept region j.
+void launch_link(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, double t,
+                 const int64_t* offsets, const double* est, const double* err,
+                 const uint8_t* axis, uint64_t* link, double* pest);
 
 // Compaction only (filter() for the batch API).
 void launch_compact(cudaStream_t st, int n, int64_t m, int64_t cap, const uint8_t* flag,
