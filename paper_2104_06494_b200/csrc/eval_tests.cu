@@ -88,7 +88,12 @@ void launch_evaluate(const EvalLaunch& k, cudaStream_t st, const EvalParams& ep)
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem));
   }
   const unsigned grid = static_cast<unsigned>((ep.m + kEvalThreads - 1) / kEvalThreads);
-  fn<<<grid, kEvalThreads, k.smem, st>>>(ep, device_exp_table(), device_sincos_table());
+  if (ep.link) {  // behind k_link: programmatic launch (pdl_wait in load_geometry)
+    PGN_CK(launch_pdl(fn, dim3(grid), dim3(kEvalThreads), k.smem, st, ep, device_exp_table(),
+                      device_sincos_table()));
+  } else {
+    fn<<<grid, kEvalThreads, k.smem, st>>>(ep, device_exp_table(), device_sincos_table());
+  }
 }
 
 }  // namespace pgn

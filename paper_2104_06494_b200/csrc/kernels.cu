@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(256)
                      ProbeScalars* out, unsigned* ready, unsigned seq, int* done) {
   const int id = blockIdx.x;  // 0..2T-1 folds, 2T..3T-1 counts
   const int tid = threadIdx.x;
+  pdl_wait();  // k_probe_multi's block records (launch_pdl)
   // zero-copy hand-off: `out` is mapped host memory; the last CTA to finish
   // publishes `seq` once every CTA's field is fenced (no D2H copy + sync)
   auto publish = [&] {
@@ -634,6 +635,7 @@ __global__ void __launch_bounds__(kFinThreads)
   __shared__ int64_t s_sum[kFinThreads];
   __shared__ unsigned long long s_k[2][kFinThreads / 32];
   const int tid = threadIdx.x;
+  pdl_wait();  // the block records of the kernel before (launch_pdl)
   if (mm) {  // min_max of the errors from per-block keys (reduce.cpp:74-82; exact)
     unsigned long long a = ~0ULL, z = 0ULL;
     for (int64_t i = tid; i < nblk; i += kFinThreads) {
@@ -1120,6 +1122,14 @@ void launch_fold_eval(cudaStream_t st, int64_t m, const double* est, const doubl
 }
 
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Opt a kernel in to > 48 KB of dynamic shared memory, once per (device, kernel).
 void opt_in_smem(const void* fn) {
   static std::mutex mu;
@@ -1138,11 +1148,11 @@ void finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
   const size_t sm = tree_smem_bytes(nblk, 1);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
     opt_in_smem(reinterpret_cast<const void*>(&k_finalize_multi<true>));
-    k_finalize_multi<true><<<3 * T, 256, sm, st>>>(nblk, T, part, cnt, scratch, out, ready, seq,
-                                                   done);
+    (void)(launch_pdl(&k_finalize_multi<true>, dim3(3 * T), dim3(256), sm, st, nblk, T, part, cnt,
+                      scratch, out, ready, seq, done));
   } else {
-    k_finalize_multi<false><<<3 * T, 256, 0, st>>>(nblk, T, part, cnt, scratch, out, ready, seq,
-                                                    done);
+    (void)(launch_pdl(&k_finalize_multi<false>, dim3(3 * T), dim3(256), 0, st, nblk, T, part, cnt,
+                      scratch, out, ready, seq, done));
   }
 }
 
@@ -1230,11 +1240,11 @@ void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
   const size_t sm = tree_smem_bytes(nblk, 4);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
     opt_in_smem(reinterpret_cast<const void*>(&k_finalize<true>));
-    k_finalize<true><<<1, kFinThreads, sm, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
-                                                 err0, ready, seq);
+    (void)(launch_pdl(&k_finalize<true>, dim3(1), dim3(kFinThreads), sm, st, nblk, nq, part, cnt,
+                      offsets, scratch, out, mm, err0, ready, seq));
   } else {
-    k_finalize<false><<<1, kFinThreads, 0, st>>>(nblk, nq, part, cnt, offsets, scratch, out, mm,
-                                                  err0, ready, seq);
+    (void)(launch_pdl(&k_finalize<false>, dim3(1), dim3(kFinThreads), 0, st, nblk, nq, part, cnt,
+                      offsets, scratch, out, mm, err0, ready, seq));
   }
 }
 
@@ -1721,55 +1731,104 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
 // the next k_evaluate derives children 2k, 2k+1 from that row
 // (geometry.cpp:122-141, evaluate.cuh load_geometry).  No geometry moves
 // here: 10-18 B read per region, 16 B written per kept region, all coalesced.
-constexpr int kLinkThreads = 512;
-constexpr int kLinkPer = static_cast<int>(kBlock) / kLinkThreads;  // 4
+constexpr int kLinkThreads = 256;
+constexpr int kLinkPer = static_cast<int>(kBlock) / kLinkThreads;  // 8 consecutive regions
 __global__ void __launch_bounds__(kLinkThreads)
     k_link(int64_t m, const uint8_t* __restrict__ flag, int use_t, double t,
            const int64_t* __restrict__ offsets, const double* __restrict__ est,
            const double* __restrict__ err, const uint8_t* __restrict__ axis,
            uint64_t* __restrict__ link, double* __restrict__ pest) {
   constexpr int W = kLinkThreads / 32;
-  __shared__ int s_cnt[kLinkPer][W];
+  __shared__ __align__(16) uint64_t s_link[kBlock];
+  __shared__ __align__(16) double s_pest[kBlock];
+  __shared__ int s_warp[W + 1];
+  pdl_trigger();  // the next k_evaluate may launch (it waits for this grid in pdl_wait)
   const int64_t b = blockIdx.x;
   const int64_t base = b * kBlock;
+  const int n = static_cast<int>(m - base < kBlock ? m - base : kBlock);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint8_t fl[kLinkPer], ax[kLinkPer];
-  double ev[kLinkPer], xv[kLinkPer];
+  const int i0 = threadIdx.x * kLinkPer;  // this thread's 8 regions: base + i0 .. + 7
+  // every load issued before any use: flag / axis as 8-byte words, est / err
+  // as 16-byte pairs (the block start is 2048-aligned, so all are aligned)
+  uint2 fw = make_uint2(0u, 0u), aw = make_uint2(0u, 0u);
+  double2 xv[kLinkPer / 2], ev[kLinkPer / 2];
+  const bool full = i0 + kLinkPer <= n;
+  if (full) {
+    fw = __ldg(reinterpret_cast<const uint2*>(flag + base + i0));
+    aw = __ldg(reinterpret_cast<const uint2*>(axis + base + i0));
 #pragma unroll
-  for (int r = 0; r < kLinkPer; ++r) {  // every load issued before any use
-    const int64_t j = base + r * kLinkThreads + threadIdx.x;
-    const bool in = j < m;
-    fl[r] = in ? __ldg(flag + j) : uint8_t{0};
-    ax[r] = in ? __ldg(axis + j) : uint8_t{0};
-    xv[r] = in ? __ldg(est + j) : 0.0;
-    ev[r] = (use_t && in) ? __ldg(err + j) : 0.0;
-  }
-  bool keep[kLinkPer];
-  unsigned before[kLinkPer];
+    for (int u = 0; u < kLinkPer / 2; ++u) {
+      xv[u] = __ldg(reinterpret_cast<const double2*>(est + base + i0) + u);
+      ev[u] = use_t ? __ldg(reinterpret_cast<const double2*>(err + base + i0) + u)
+                    : make_double2(0.0, 0.0);
+    }
+  } else {  // the batch's ragged last block
+    uint8_t fb[kLinkPer] = {}, ab[kLinkPer] = {};
+    double xs[kLinkPer] = {}, es[kLinkPer] = {};
 #pragma unroll
-  for (int r = 0; r < kLinkPer; ++r) {
-    keep[r] = fl[r] != 0 && !(use_t && ev[r] < t);
-    const unsigned bal = __ballot_sync(0xffffffffu, keep[r]);
-    before[r] = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 0) s_cnt[r][wid] = __popc(bal);
+    for (int u = 0; u < kLinkPer; ++u)
+      if (i0 + u < n) {
+        fb[u] = __ldg(flag + base + i0 + u);
+        ab[u] = __ldg(axis + base + i0 + u);
+        xs[u] = __ldg(est + base + i0 + u);
+        if (use_t) es[u] = __ldg(err + base + i0 + u);
+      }
+#pragma unroll
+    for (int u = 0; u < kLinkPer; ++u) {
+      (u < 4 ? fw.x : fw.y) |= static_cast<unsigned>(fb[u]) << (8 * (u & 3));
+      (u < 4 ? aw.x : aw.y) |= static_cast<unsigned>(ab[u]) << (8 * (u & 3));
+    }
+#pragma unroll
+    for (int u = 0; u < kLinkPer / 2; ++u) {
+      xv[u] = make_double2(xs[2 * u], xs[2 * u + 1]);
+      ev[u] = make_double2(es[2 * u], es[2 * u + 1]);
+    }
   }
+  // kept = flag && !(use_t && err < t) (classify.cpp:63-66)
+  unsigned keep = 0;
+#pragma unroll
+  for (int u = 0; u < kLinkPer; ++u) {
+    const unsigned f = ((u < 4 ? fw.x : fw.y) >> (8 * (u & 3))) & 0xffu;
+    const double e = (u & 1) ? ev[u / 2].y : ev[u / 2].x;
+    keep |= (f != 0 && !(use_t && e < t)) ? (1u << u) : 0u;
+  }
+  // rank of the thread's first kept region in the block: warp scan + block scan
+  const int c = __popc(keep);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
   __syncthreads();
-  int64_t run = offsets[b];
-#pragma unroll
-  for (int r = 0; r < kLinkPer; ++r) {
-    int wbase = 0, total = 0;
+  if (threadIdx.x == 0) {
+    int run = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const int c = s_cnt[r][w];
-      wbase += w < wid ? c : 0;
-      total += c;
+      const int v = s_warp[w];
+      s_warp[w] = run;
+      run += v;
     }
-    const int64_t k = run + wbase + before[r];
-    run += total;
-    if (!keep[r]) continue;
-    const int64_t j = base + r * kLinkThreads + threadIdx.x;
-    link[k] = static_cast<uint64_t>(j) | (static_cast<uint64_t>(ax[r]) << 56);
-    pest[k] = xv[r];
+    s_warp[W] = run;
+  }
+  __syncthreads();
+  int r = s_warp[wid] + incl - c;
+  // stage the block's entries in rank order, then write them out coalesced
+#pragma unroll
+  for (int u = 0; u < kLinkPer; ++u) {
+    if (!((keep >> u) & 1u)) continue;
+    const unsigned ax = ((u < 4 ? aw.x : aw.y) >> (8 * (u & 3))) & 0xffu;
+    s_link[r] = static_cast<uint64_t>(base + i0 + u) | (static_cast<uint64_t>(ax) << 56);
+    s_pest[r] = (u & 1) ? xv[u / 2].y : xv[u / 2].x;
+    ++r;
+  }
+  __syncthreads();
+  const int total = s_warp[W];
+  const int64_t k0 = offsets[b];
+  for (int i = threadIdx.x; i < total; i += kLinkThreads) {
+    link[k0 + i] = s_link[i];
+    pest[k0 + i] = s_pest[i];
   }
 }
 

@@ -18,6 +18,25 @@ constexpr int64_t kBlock = 2048;
 
 inline int64_t nblocks_of(int64_t m) { return (m + kBlock - 1) / kBlock; }
 
+// Launch with programmatic stream serialization (the kernel calls pdl_wait()
+// before touching its predecessor's outputs); PAGANI_PDL=0 launches plainly.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Scalars produced by k_finalize (device) and copied to pinned host memory.
 struct FoldScalars {
   double sum[4];
