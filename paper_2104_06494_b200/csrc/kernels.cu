@@ -199,6 +199,12 @@ constexpr int kProbeThreads = 128;
 #endif
 constexpr int kProbeUnroll = PGN_PROBE_UNROLL;
 constexpr int kProbeChunk = 384;  // = 4 x 96 producer threads = 3 x 128
+#ifndef PGN_PROBE_LDS_PIPE
+#define PGN_PROBE_LDS_PIPE 1
+#endif
+#ifndef PGN_PROBE_PIPE
+#define PGN_PROBE_PIPE 1  // producers keep the next chunk's loads in flight across a barrier
+#endif
 struct ProbeStage {
   double err[2][kProbeChunk];
   double est[2][kProbeChunk];
@@ -220,40 +226,60 @@ __device__ __forceinline__ uint8_t probe_code(const double* ss, int nan_cnt, uin
 }
 
 // Stage chunk c (kProbeChunk regions) into ring slot c & 1: nt threads, PER
-// regions each (nt * PER == kProbeChunk); all loads are issued before any use.
+// regions each (nt * PER == kProbeChunk).  Split in two halves so the
+// producers can software-pipeline: probe_load issues the chunk's global loads
+// into registers, probe_store (one barrier interval later) turns them into
+// codes + ring entries -- the loads of chunk c + 2 are in flight while the
+// folding warp works through chunk c.
+template <int PER>
+struct ProbeRegs {
+  double e[PER], v[PER];
+  uint8_t f[PER];
+};
+template <int PER>
+__device__ __forceinline__ void probe_load(ProbeRegs<PER>& R, const double* __restrict__ est,
+                                           const double* __restrict__ err,
+                                           const uint8_t* __restrict__ flag, int64_t lo, int n,
+                                           int c, int t0, int nt) {
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = c * kProbeChunk + t0 + u * nt;
+    R.e[u] = 0.0;
+    R.v[u] = 0.0;
+    R.f[u] = 0;
+    if (k < n) {
+      R.e[u] = __ldg(err + lo + k);
+      R.v[u] = __ldg(est + lo + k);
+      R.f[u] = __ldg(flag + lo + k);
+    }
+  }
+}
+template <int PER>
+__device__ __forceinline__ void probe_store(ProbeStage& S, const ProbeSet& ts,
+                                            const ProbeRegs<PER>& R, int c, int t0, int nt) {
+  const int buf = c & 1;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = t0 + u * nt;
+    const uint8_t code = probe_code(S.s, ts.nan_cnt, R.f[u], R.e[u]);
+    // one shared atomic per distinct code in the warp (padding regions past
+    // the block end have code 0, which no count reads)
+    const unsigned peers = __match_any_sync(0xffffffffu, static_cast<unsigned>(code));
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&S.hist[code], __popc(peers));
+    S.err[buf][i] = R.e[u];
+    S.est[buf][i] = R.v[u];
+    S.mask[buf][i] = static_cast<uint16_t>((1u << code) - 1u);
+  }
+}
 template <int PER>
 __device__ __forceinline__ void probe_stage_chunk(ProbeStage& S, const ProbeSet& ts,
                                                   const double* __restrict__ est,
                                                   const double* __restrict__ err,
                                                   const uint8_t* __restrict__ flag, int64_t lo,
                                                   int n, int c, int t0, int nt) {
-  const int buf = c & 1;
-  double e[PER], v[PER];
-  uint8_t f[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int k = c * kProbeChunk + t0 + u * nt;
-    e[u] = 0.0;
-    v[u] = 0.0;
-    f[u] = 0;
-    if (k < n) {
-      e[u] = __ldg(err + lo + k);
-      v[u] = __ldg(est + lo + k);
-      f[u] = __ldg(flag + lo + k);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int i = t0 + u * nt;
-    const uint8_t code = probe_code(S.s, ts.nan_cnt, f[u], e[u]);
-    // one shared atomic per distinct code in the warp (padding regions past
-    // the block end have code 0, which no count reads)
-    const unsigned peers = __match_any_sync(0xffffffffu, static_cast<unsigned>(code));
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&S.hist[code], __popc(peers));
-    S.err[buf][i] = e[u];
-    S.est[buf][i] = v[u];
-    S.mask[buf][i] = static_cast<uint16_t>((1u << code) - 1u);
-  }
+  ProbeRegs<PER> R;
+  probe_load<PER>(R, est, err, flag, lo, n, c, t0, nt);
+  probe_store<PER>(S, ts, R, c, t0, nt);
 }
 
 // s += v unless (word & bit): the skip of reduce.cpp:59-60 as a predicated
@@ -292,11 +318,19 @@ __global__ void __launch_bounds__(kProbeThreads)
   const int pos = ts.pos[node];
   const int q = lane >> 4;  // 0: err chain, 1: est chain
   double fin = 0.0;
+  constexpr int kPer = kProbeChunk / (kProbeThreads - 32);
+  ProbeRegs<kPer> R;  // producers: chunk c + 1's loads, stored one interval later
+  if (w > 0 && nch > 1) probe_load<kPer>(R, est, err, flag, lo, n, 1, tid - 32, kProbeThreads - 32);
   for (int c = 0; c < nch; ++c) {
     if (w > 0) {
-      if (c + 1 < nch)
-        probe_stage_chunk<kProbeChunk / (kProbeThreads - 32)>(S, ts, est, err, flag, lo, n, c + 1,
-                                                              tid - 32, kProbeThreads - 32);
+      if (c + 1 < nch) {
+#if PGN_PROBE_PIPE
+        probe_store<kPer>(S, ts, R, c + 1, tid - 32, kProbeThreads - 32);
+        if (c + 2 < nch) probe_load<kPer>(R, est, err, flag, lo, n, c + 2, tid - 32, kProbeThreads - 32);
+#else
+        probe_stage_chunk<kPer>(S, ts, est, err, flag, lo, n, c + 1, tid - 32, kProbeThreads - 32);
+#endif
+      }
     } else {
       const int buf = c & 1;
       const double* x = q ? S.est[buf] : S.err[buf];
@@ -304,6 +338,38 @@ __global__ void __launch_bounds__(kProbeThreads)
       const int cntc = n - c * kProbeChunk < kProbeChunk ? n - c * kProbeChunk : kProbeChunk;
       if (cntc == kProbeChunk) {
         const uint32_t blo = 1u << pos, bhi = blo << 16;
+#if PGN_PROBE_LDS_PIPE
+        // register double buffer: group g + 1's shared-memory loads are issued
+        // before group g's 8 dependent DADDs, so with one or two folding warps
+        // per SM sub-partition the LDS latency is off the chain
+        uint4 m8 = *reinterpret_cast<const uint4*>(mk);
+        double2 v0 = *reinterpret_cast<const double2*>(x);
+        double2 v1 = *reinterpret_cast<const double2*>(x + 2);
+        double2 v2 = *reinterpret_cast<const double2*>(x + 4);
+        double2 v3 = *reinterpret_cast<const double2*>(x + 6);
+#pragma unroll 2
+        for (int i = 0; i < kProbeChunk; i += 8) {
+          const int nx = i + 8 < kProbeChunk ? i + 8 : i;  // last group: harmless reload
+          const uint4 n8 = *reinterpret_cast<const uint4*>(mk + nx);
+          const double2 n0 = *reinterpret_cast<const double2*>(x + nx);
+          const double2 n1 = *reinterpret_cast<const double2*>(x + nx + 2);
+          const double2 n2 = *reinterpret_cast<const double2*>(x + nx + 4);
+          const double2 n3 = *reinterpret_cast<const double2*>(x + nx + 6);
+          add_unless(fin, v0.x, m8.x, blo);
+          add_unless(fin, v0.y, m8.x, bhi);
+          add_unless(fin, v1.x, m8.y, blo);
+          add_unless(fin, v1.y, m8.y, bhi);
+          add_unless(fin, v2.x, m8.z, blo);
+          add_unless(fin, v2.y, m8.z, bhi);
+          add_unless(fin, v3.x, m8.w, blo);
+          add_unless(fin, v3.y, m8.w, bhi);
+          m8 = n8;
+          v0 = n0;
+          v1 = n1;
+          v2 = n2;
+          v3 = n3;
+        }
+#else
 #pragma unroll kProbeUnroll
         for (int i = 0; i < kProbeChunk; i += 8) {
           const uint4 m8 = *reinterpret_cast<const uint4*>(mk + i);
@@ -320,6 +386,7 @@ __global__ void __launch_bounds__(kProbeThreads)
           add_unless(fin, v3.x, m8.w, blo);
           add_unless(fin, v3.y, m8.w, bhi);
         }
+#endif
       } else {
         for (int i = 0; i < cntc; ++i) add_unless(fin, x[i], mk[i], 1u << pos);
       }
