@@ -138,7 +138,10 @@ typedef struct pagani_config {
   /* B200 extensions */
   int32_t mode;                 /* PAGANI_MODE_* */
   int32_t device;               /* CUDA device ordinal (single-process) */
-  int32_t profile;              /* 1 = record per-kernel CUDA-event times */
+  int32_t profile;              /* 1 = record per-kernel CUDA-event times; 2 = k_evaluate's
+                                   only (two event records per iteration instead of ~8:
+                                   the host-side record calls sit on the GPU's critical path
+                                   between host decisions and the next launch) */
   int32_t reserved0;
   /* per-iteration trace callback (full-precision BFCUB_TRACE, driver.cpp:174-182) */
   void (*trace)(const struct pagani_trace_row* row, void* user);
@@ -193,6 +196,11 @@ typedef struct pagani_result {
   /* Algorithmic HBM bytes per kernel kind (what each launch must read and
    * write), for the HBM rooflines of the memory kernels. */
   double kernel_bytes[PAGANI_N_KERNEL_SLOTS];
+  /* Speculative first threshold passes: launched behind
+   * k_finalize before the host decided whether a search runs, and how many of
+   * them ran for nothing (no search that iteration). */
+  int32_t spec_probe_passes;
+  int32_t spec_probe_wasted;
 } pagani_result;
 
 /* One row per iteration (the BFCUB_TRACE point, driver.cpp:174-182, in full

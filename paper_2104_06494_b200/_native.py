@@ -94,7 +94,8 @@ class Result(C.Structure):
                 ("region_evals", C.c_int64), ("peak_regions", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("device_ms", C.c_double),
-                ("kernel_bytes", C.c_double * PAGANI_N_KERNEL_SLOTS)]
+                ("kernel_bytes", C.c_double * PAGANI_N_KERNEL_SLOTS),
+                ("spec_probe_passes", C.c_int32), ("spec_probe_wasted", C.c_int32)]
 
 
 class ThresholdResult(C.Structure):

@@ -123,7 +123,7 @@ class Config:
     threshold_limits: ThresholdLimits = field(default_factory=ThresholdLimits)
     mode: str = "parity"  # "parity" (bit-exact) | "fast"
     device: int = 0
-    profile: bool = False
+    profile: int = 0  # 1 (or True): every kernel class timed; 2: k_evaluate only (cheap)
     comm: object = None  # dist.Communicator for multi-GPU runs (one process per GPU)
 
     def convergence_digits(self) -> int:  # driver.cpp:28-33
@@ -154,7 +154,7 @@ class Config:
         c.p_max_start, c.p_max_step, c.p_max_cap = L.p_max_start, L.p_max_step, L.p_max_cap
         c.mode = {"parity": N.MODE_PARITY, "fast": N.MODE_FAST}[self.mode]
         c.device = self.device
-        c.profile = int(bool(self.profile))
+        c.profile = int(self.profile) if not isinstance(self.profile, bool) else int(self.profile)
         c.comm = self.comm.handle if self.comm is not None else None
         return c
 
@@ -194,6 +194,8 @@ class IntegrationResult:
     device_ms: float = 0.0
     probe_fallbacks: int = 0  # streamed threshold passes re-run exactly
     trace: Optional[list] = None
+    spec_probe_passes: int = 0  # first passes queued behind k_finalize
+    spec_probe_wasted: int = 0  # ... of which no search used
 
 
 # ----------------------------------------------------------- integrands ----
@@ -311,7 +313,8 @@ def integrate(f, bounds: Bounds, config: Optional[Config] = None,
         kernel_bytes={k: out.kernel_bytes[i] for i, k in enumerate(N.KERNEL_SLOTS)},
         region_evals=out.region_evals, peak_regions=out.peak_regions,
         h2d_bytes=out.h2d_bytes, d2h_bytes=out.d2h_bytes, device_ms=out.device_ms,
-        probe_fallbacks=out.probe_fallbacks, trace=rows if trace else None)
+        probe_fallbacks=out.probe_fallbacks, trace=rows if trace else None,
+        spec_probe_passes=out.spec_probe_passes, spec_probe_wasted=out.spec_probe_wasted)
 
 
 def integrate_sequential(f, bounds: Bounds, tau_rel: float, tau_abs: float = 1e-20,

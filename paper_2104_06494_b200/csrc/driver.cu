@@ -86,6 +86,7 @@ void Workspace::ensure(int n_, int64_t cap_) {
     PGN_CK(cudaMallocHost(&h_probe, sizeof(ProbeScalars)));
     PGN_CK(cudaHostAlloc(&h_probe_zc, sizeof(ProbeScalars), cudaHostAllocMapped));
     PGN_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_probe_zc), h_probe_zc, 0));
+    spec_ps.alloc(1);
     probe_done.alloc(1);
     PGN_CK(cudaMemset(probe_done.p, 0, sizeof(int)));
     PGN_CK(cudaHostAlloc(&h_zc, sizeof(FoldScalars), cudaHostAllocMapped));
@@ -260,6 +261,20 @@ bool probe_stream() {
 
 // Deferred bisection on one GPU (k_link + children derived in k_evaluate,
 // DESIGN.md 4); PAGANI_DEFER_BISECT=0 selects the explicit split kernel.
+// Speculative first probe pass: after an iteration that ran a
+// threshold search, the next iteration's first pass is queued behind
+// k_finalize, its thresholds built on the device.  Opt-in
+// (PAGANI_SPEC_PROBE=1): bit-identical, but measured neutral on B200 (bench
+// step 2034 vs 2032 ms) -- the host round trip it hides is about what the
+// wasted passes (7% of them) and the serial build in k_finalize cost.
+bool spec_probe() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_SPEC_PROBE");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool defer_bisect() {
   static const bool on = [] {
     const char* e = std::getenv("PAGANI_DEFER_BISECT");
@@ -320,13 +335,16 @@ int initial_subdivisions(int n, int64_t init_target) {  // geometry.cpp:67-81
 // hand-off), checking the stream for errors now and then so a failed launch
 // cannot hang the host.
 void wait_host_flag(const unsigned* flag, unsigned seq, cudaStream_t st) {
+  // `seq` or later: a kernel queued behind the awaited one (the speculative
+  // first probe pass) may already have published the next number
   const volatile unsigned* f = flag;
+  auto reached = [&] { return static_cast<int>(*f - seq) >= 0; };
   for (uint64_t i = 0;; ++i) {
-    if (*f == seq) break;
+    if (reached()) break;
     if ((i & 4095) == 4095) {
       const cudaError_t e = cudaStreamQuery(st);
       if (e == cudaSuccess) {
-        if (*f == seq) break;
+        if (reached()) break;
         throw CudaError("zero-copy hand-off: stream idle but the scalars were not published");
       }
       if (e != cudaErrorNotReady) cuda_check(e, "k_finalize (zero-copy hand-off)");
@@ -341,7 +359,7 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
                                   const Limits& lim, double* probe_ms, const double* minmax,
-                                  ShardCtx* sh) {
+                                  ShardCtx* sh, unsigned spec_seq) {
   ThresholdOutcome r;
   if (s_it <= 0) return r;
   const double e_budget = e_tot - std::fabs(v_tot) * tau_rel;
@@ -490,6 +508,33 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
         return r;
       }
     }
+    if (!decided && spec_seq != 0 && r.passes == 0) {
+      // the first pass already ran on the device, queued right behind
+      // k_finalize with the ProbeSet it built from the same scalars by the
+      // same code (build_probe_tree; event 0 was recorded before it)
+      r.spec_used = true;
+      r.bytes += 17.0 * m;
+      timed_wait(spec_seq);
+      *ws.h_probe = *ws.h_probe_zc;
+      decided = true;
+      const ProbeScalars& pr = *ws.h_probe;
+      replay(ps, pr, false, w);
+      if (w.accepted >= 0) {
+        const int node = w.accepted;
+        r.success = true;
+        r.threshold = ps.t[node];
+        r.discarded = pr.err_sum[node];
+        r.budget_limit = w.p_max * e_budget;
+        r.finished_count = s_it - pr.count[node];
+        r.fin_v = pr.est_sum[node];
+        r.node = node;
+        r.attempts = w.attempts;
+        r.direction_changes = w.direction_changes;
+        launch_scan_counts(st, nblk, ws.cnt_multi.p + node * nblk, ws.off_probe.p);
+        return r;
+      }
+      continue;
+    }
     if (!decided) {  // the exact pass: the strict folds of every node
       if (probe_ms) PGN_CK(cudaEventRecord(e0, st));
       // zero-copy hand-off of the pass results (as k_finalize's scalars): the
@@ -578,21 +623,28 @@ constexpr size_t kSpanBegin = 2, kSpanEnd = 3, kFirstMark = 4;
 
 struct KTimer {
   Workspace& ws;
-  bool on;
+  bool on;         // profile 1: every kernel class
+  bool eval_only;  // profile 2: k_evaluate's span only
   std::vector<std::pair<int, std::pair<size_t, size_t>>> spans;
   size_t next = kFirstMark;
-  KTimer(Workspace& w, bool o) : ws(w), on(o) {}
+  KTimer(Workspace& w, int level) : ws(w), on(level == 1), eval_only(level == 2) {}
   size_t mark() {
     if (!on) return 0;
     const size_t i = next++;
     PGN_CK(cudaEventRecord(ws.event(i), ws.st));
     return i;
   }
+  size_t mark_eval() {  // the marks around k_evaluate: recorded at either level
+    if (!on && !eval_only) return 0;
+    const size_t i = next++;
+    PGN_CK(cudaEventRecord(ws.event(i), ws.st));
+    return i;
+  }
   void span(int slot, size_t a, size_t b) {
-    if (on) spans.push_back({slot, {a, b}});
+    if ((on || eval_only) && a != 0 && b != 0) spans.push_back({slot, {a, b}});
   }
   void collect(pagani_result* out) {
-    if (!on) return;
+    if (!on && !eval_only) return;
     for (auto& s : spans) {
       float ms = 0;
       PGN_CK(cudaEventElapsedTime(&ms, ws.event(s.second.first), ws.event(s.second.second)));
@@ -682,8 +734,8 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
   }
   const int64_t cap = ws.cap;
   int64_t m = sh ? sh->local() : M;  // local batch size
-  const bool prof = cfg.profile != 0;
-  KTimer kt(ws, prof);
+  const bool prof = cfg.profile == 1;
+  KTimer kt(ws, cfg.profile);
   cudaEvent_t ev_begin = ws.event(kSpanBegin), ev_end = ws.event(kSpanEnd);
   PGN_CK(cudaEventRecord(ev_begin, st));
 
@@ -766,6 +818,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
 
   bool done = false;
   bool linked = false;  // this batch's geometry still lives in its parents' rows (k_link)
+  bool searched_last = false;  // the previous iteration ran a threshold search
   for (int it = 1; it <= cfg.it_max && !done; ++it) {
     // ---- evaluate (+ refine + classify + block folds) -------------------------
     ep.m = m;
@@ -777,7 +830,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     ep.plow = linked ? ws.low[cur ^ 1].p : nullptr;
     ep.plen = linked ? ws.len[cur ^ 1].p : nullptr;
     ep.refine = (it > 1 && cfg.refiner == PAGANI_REFINER_TWO_LEVEL) ? 1 : 0;
-    const size_t k0 = kt.mark();
+    const size_t k0 = kt.mark_eval();
     const int64_t nblk = nblocks_of(m);
     ep.nblk = nblk;
     if (eval_k.fused_fold) {  // block folds + min/max run in k_evaluate's tail
@@ -790,7 +843,7 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       launch_evaluate(eval_k, st, ep);
       PGN_CK(cudaGetLastError());
     }
-    const size_t k1 = kt.mark();
+    const size_t k1 = kt.mark_eval();
     kt.span(PAGANI_K_EVALUATE, k0, k1);
     out->kernel_launches[PAGANI_K_EVALUATE] += m > 0;
     // reads low/len (16n) [+ pest 8], writes est, err (16) + flag, axis (2)
@@ -809,11 +862,30 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     }
     const size_t k2 = kt.mark();
     const int64_t* offsets = ws.off_eval.p;  // kept offsets, indexed by (global) block
+    // the next search's first pass, queued behind k_finalize before the host
+    // has decided whether a search runs (it usually does once one has)
+    const bool spec = !sh && eval_k.fused_fold && searched_last && it < cfg.it_max && m > 0 &&
+                      spec_probe() && !probe_stream();
+    unsigned spec_seq = 0;
+    size_t sx0 = 0, sx1 = 0, k3 = 0;
     if (!sh) {
+      SpecProbe sp;
+      if (spec) sp = SpecProbe{ws.spec_ps.p, M};
       launch_finalize(st, nblk, 4, ws.part_eval.p, ws.cnt_eval.p, ws.off_eval.p, ws.scratch.p,
                       ws.d_zc, eval_k.fused_fold ? ws.mm_blk.p : nullptr, ws.err.p, ws.d_ready,
-                      ++ws.seq);
+                      ++ws.seq, sp);
       out->kernel_launches[PAGANI_K_FINALIZE]++;
+      k3 = kt.mark();
+      if (spec) {
+        sx0 = k3;
+        if (prof) PGN_CK(cudaEventRecord(ws.event(0), st));  // device_threshold's pass timer
+        spec_seq = ++ws.seq;
+        out->spec_probe_passes++;
+        launch_probe_multi_dev(st, m, ws.spec_ps.p, ws.est.p, ws.err.p, ws.flag.p,
+                               ws.part_multi.p, ws.cnt_multi.p, ws.scratch_multi.p,
+                               ws.d_probe_zc, ws.d_ready, spec_seq, ws.probe_done.p);
+        sx1 = kt.mark();
+      }
     } else {  // allgather the block records; every rank runs the same global trees
       launch_pack_blocks(st, nblk, sh->nblk_max, ws.part_eval.p, ws.cnt_eval.p, ws.mm_blk.p,
                          ws.err.p, ws.rec_send.p);
@@ -830,10 +902,10 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
       out->kernel_launches[PAGANI_K_FINALIZE] += 4;
       offsets = ws.g_off.p;
     }
-    const size_t k3 = kt.mark();
+    if (sh) k3 = kt.mark();
     kt.span(PAGANI_K_FOLD, k1, k2);
     kt.span(PAGANI_K_FINALIZE, k2, k3);
-    wait_host_flag(ws.h_ready, ws.seq, st);
+    wait_host_flag(ws.h_ready, spec ? spec_seq - 1 : ws.seq, st);
     ws.h_sc[0] = *ws.h_zc;
     out->d2h_bytes += sizeof(FoldScalars);
     if (sh) {
@@ -886,12 +958,16 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
     double t_accepted = 0.0;
     double fin_v = sc.sum[2], fin_e = sc.sum[3];
     int64_t kept = sc.count;
+    bool spec_used = false;
+    searched_last = trig_digits || trig_memory;
     if (trig_digits || trig_memory) {
       double pms = 0.0;
       const double known_mm[2] = {sc.mn, sc.mx};
       const ThresholdOutcome tr = device_threshold(
           ws, m, ws.est.p, ws.err.p, ws.flag.p, acc_v + acc_vf, acc_e + acc_ef, acc_e, M,
-          cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr, sh);
+          cfg.tau_rel, lim, prof ? &pms : nullptr, eval_k.fused_fold ? known_mm : nullptr, sh,
+          spec_seq);
+      spec_used = tr.spec_used;
       out->kernel_ms[PAGANI_K_PROBE] += pms;
       out->kernel_bytes[PAGANI_K_PROBE] += tr.bytes;
       out->kernel_launches[PAGANI_K_PROBE] += (sh ? 5 : 2) * tr.passes + (tr.success ? 1 : 0);
@@ -932,6 +1008,12 @@ void integrate(const pagani_integrand* f, int ndim, const double* lower, const d
           for (int r = 0; r <= R; ++r) kb[r] = ws.h_kb[r];
         }
       }
+    }
+    if (spec && !spec_used) {  // the speculative pass ran for nothing: account for it
+      kt.span(PAGANI_K_PROBE, sx0, sx1);
+      out->kernel_launches[PAGANI_K_PROBE] += 2;
+      out->kernel_bytes[PAGANI_K_PROBE] += 17.0 * static_cast<double>(m);
+      out->spec_probe_wasted++;
     }
     row.v = acc_v, row.e = acc_e, row.v_f = acc_vf, row.e_f = acc_ef;
     row.active_final = kept;

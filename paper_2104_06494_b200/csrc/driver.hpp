@@ -74,6 +74,7 @@ struct Workspace {
   ProbeScalars* h_probe = nullptr;      // pinned
   ProbeScalars* h_probe_zc = nullptr;   // mapped: zero-copy pass results
   ProbeScalars* d_probe_zc = nullptr;   // device alias of h_probe_zc
+  DevBuf<ProbeSet> spec_ps;  // the speculative first pass's thresholds (k_finalize builds them)
   DevBuf<int> probe_done;               // k_finalize_multi's CTA arrival counter
   // multi-GPU (sharded) buffers: global-order block arrays, records, staging
   int64_t nb_global_cap = 0, stage_cap = 0;
@@ -134,6 +135,7 @@ struct ThresholdOutcome {
   int passes = 0;           // speculative probe passes (2 kernels + 1 D2H each)
   int node = -1;            // accepted node of the last pass
   int exact_fallbacks = 0;  // streamed passes too close to call (re-run exactly)
+  bool spec_used = false;   // the first pass was the speculative one
   double bytes = 0.0;       // algorithmic HBM bytes read by the search's kernels
 };
 
@@ -162,7 +164,8 @@ ThresholdOutcome device_threshold(Workspace& ws, int64_t m, const double* d_est,
                                   const double* d_err, const uint8_t* d_flag, double v_tot,
                                   double e_tot, double e_it, int64_t s_it, double tau_rel,
                                   const Limits& lim, double* probe_ms,
-                                  const double* minmax = nullptr, ShardCtx* sh = nullptr);
+                                  const double* minmax = nullptr, ShardCtx* sh = nullptr,
+                                  unsigned spec_seq = 0);
 
 void integrate(const pagani_integrand* f, int ndim, const double* lower, const double* upper,
                const pagani_config* cfg, pagani_result* out);

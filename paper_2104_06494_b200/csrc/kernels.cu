@@ -299,10 +299,14 @@ __device__ __forceinline__ void add_unless(double& s, double v, uint32_t word, u
 }
 
 __global__ void __launch_bounds__(kProbeThreads)
-    k_probe_multi(int64_t m, int64_t nblk, const ProbeSet ts, const double* __restrict__ est,
+    k_probe_multi(int64_t m, int64_t nblk, const ProbeSet ts_arg, const double* __restrict__ est,
                   const double* __restrict__ err, const uint8_t* __restrict__ flag, double* part,
-                  int64_t* cnt) {
+                  int64_t* cnt, const ProbeSet* dts) {
   __shared__ __align__(16) ProbeStage S;
+  // dts: the speculative first pass, its ProbeSet built by k_finalize (the
+  // predecessor of this programmatic launch)
+  pdl_wait();
+  const ProbeSet& ts = dts ? *dts : ts_arg;
   const int64_t b = blockIdx.x;
   const int64_t lo = b * kBlock;
   const int n = static_cast<int>(m - lo < kBlock ? m - lo : kBlock);
@@ -693,11 +697,35 @@ __device__ __forceinline__ void signal_host(unsigned* ready, unsigned seq) {
   }
 }
 
+// prepare_probes on the device: the same sorted thresholds / positions
+// (insertion sort; the order among equal thresholds differs from std::sort's
+// but equal thresholds have the same candidates, so every code test agrees).
+__device__ void prepare_probes_dev(ProbeSet& ps) {
+  int idx[kMaxProbes];
+  int nn = 0, nf = 0;
+  for (int j = 0; j < ps.T; ++j)
+    if (ps.t[j] != ps.t[j]) ps.pos[j] = nn++;
+  for (int j = 0; j < ps.T; ++j)
+    if (ps.t[j] == ps.t[j]) {
+      int k = nf++;
+      while (k > 0 && ps.t[j] < ps.t[idx[k - 1]]) {
+        idx[k] = idx[k - 1];
+        --k;
+      }
+      idx[k] = j;
+    }
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  for (int k = 0; k < 16; ++k) ps.s[k] = k < nf ? ps.t[idx[k]] : qnan;
+  for (int k = 0; k < nf; ++k) ps.pos[idx[k]] = nn + k;
+  ps.nan_cnt = nn;
+}
+
 template <bool SMEM>
 __global__ void __launch_bounds__(kFinThreads)
     k_finalize(int64_t nblk, int nq, const double* part, const int64_t* cnt, int64_t* offsets,
                double* scratch, FoldScalars* out, const unsigned long long* mm,
-               const double* err0, unsigned* ready, unsigned seq) {
+               const double* err0, unsigned* ready, unsigned seq, SpecProbe spec) {
+  __shared__ double s_res[3];  // sum err, min, max (for the speculative first pass)
   extern __shared__ double s_tree[];
   __shared__ int64_t s_sum[kFinThreads];
   __shared__ unsigned long long s_k[2][kFinThreads / 32];
@@ -733,6 +761,8 @@ __global__ void __launch_bounds__(kFinThreads)
         out->mn = key_val(a);
         out->mx = key_val(z);
       }
+      s_res[1] = out->mn;
+      s_res[2] = out->mx;
     }
   }
   // reduce.cpp:13-27: p[i] = p[2i] + p[2i+1] level by level, odd tail carried.
@@ -742,6 +772,7 @@ __global__ void __launch_bounds__(kFinThreads)
     const double v = tree_sum_smem(part + (q < nq ? q : 0) * nblk, nblk,
                                    s_tree + q * (nblk + 64), tid % G, G);
     if (q < nq && tid % G == 0) out->sum[q] = v;
+    if (q == 1 && tid % G == 0) s_res[0] = v;
     __syncthreads();
   } else
   for (int q = 0; q < nq; ++q) {
@@ -760,6 +791,7 @@ __global__ void __launch_bounds__(kFinThreads)
       cur = half + (cur & 1);
     }
     if (tid == 0) out->sum[q] = nblk ? src[0] : 0.0;
+    if (tid == 0 && q == 1) s_res[0] = nblk ? src[0] : 0.0;
     __syncthreads();
   }
   if (!cnt) {
@@ -788,6 +820,15 @@ __global__ void __launch_bounds__(kFinThreads)
     }
   if (tid == kFinThreads - 1) out->count = s_sum[tid];
   signal_host(ready, seq);
+  if (spec.dev && mm && tid == 0) {
+    // after the host has its scalars: the next search's first pass, built
+    // from this iteration's e (the block-tree sum of the errors), batch size
+    // and error min / max exactly as device_threshold builds it on the host
+    ProbeSet ps{};
+    build_probe_tree(ps, P_DIV(s_res[0], static_cast<double>(spec.s_it)), s_res[1], s_res[2]);
+    prepare_probes_dev(ps);
+    *spec.dev = ps;
+  }
 }
 
 // ---- min / max ---------------------------------------------------------------
@@ -1242,7 +1283,7 @@ void launch_probe_only(cudaStream_t st, int64_t m, const ProbeSet& ts, const dou
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
-                                                                        flag, part, cnt);
+                                                                        flag, part, cnt, nullptr);
 }
 
 void launch_finalize_multi(cudaStream_t st, int64_t nblk, int T, const double* part,
@@ -1258,8 +1299,19 @@ void launch_probe_multi(cudaStream_t st, int64_t m, const ProbeSet& ts, const do
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
   k_probe_multi<<<static_cast<unsigned>(nblk), kProbeThreads, 0, st>>>(m, nblk, ts, est, err,
-                                                                        flag, part, cnt);
+                                                                        flag, part, cnt, nullptr);
   finalize_multi(st, nblk, ts.T, part, cnt, scratch, out, ready, seq, done);
+}
+
+void launch_probe_multi_dev(cudaStream_t st, int64_t m, const ProbeSet* dts, const double* est,
+                            const double* err, const uint8_t* flag, double* part, int64_t* cnt,
+                            double* scratch, ProbeScalars* out, unsigned* ready, unsigned seq,
+                            int* done) {
+  const int64_t nblk = nblocks_of(m);
+  if (nblk == 0) return;
+  (void)(launch_pdl(&k_probe_multi, dim3(static_cast<unsigned>(nblk)), dim3(kProbeThreads), 0, st,
+                    m, nblk, ProbeSet{}, est, err, flag, part, cnt, dts));
+  finalize_multi(st, nblk, kMaxProbes, part, cnt, scratch, out, ready, seq, done);
 }
 
 int probe_fast_grid(int64_t m) {
@@ -1303,15 +1355,15 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
                      const unsigned long long* mm, const double* err0, unsigned* ready,
-                     unsigned seq) {
+                     unsigned seq, const SpecProbe& spec) {
   const size_t sm = tree_smem_bytes(nblk, 4);
   if (sm <= static_cast<size_t>(kTreeSmemMaxBytes)) {
     opt_in_smem(reinterpret_cast<const void*>(&k_finalize<true>));
     (void)(launch_pdl(&k_finalize<true>, dim3(1), dim3(kFinThreads), sm, st, nblk, nq, part, cnt,
-                      offsets, scratch, out, mm, err0, ready, seq));
+                      offsets, scratch, out, mm, err0, ready, seq, spec));
   } else {
     (void)(launch_pdl(&k_finalize<false>, dim3(1), dim3(kFinThreads), 0, st, nblk, nq, part, cnt,
-                      offsets, scratch, out, mm, err0, ready, seq));
+                      offsets, scratch, out, mm, err0, ready, seq, spec));
   }
 }
 

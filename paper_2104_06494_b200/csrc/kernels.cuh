@@ -61,6 +61,26 @@ struct ProbeSet {
 };
 // Host: sort the node thresholds into ps.s / ps.pos / ps.nan_cnt.
 void prepare_probes(ProbeSet& ps);
+
+// The first pass of a search (classify.cpp:61-89): root t0 = e_it / s_it and
+// the depth-4 subtree of its next steps, (t + max) / 2 toward max and
+// (t + min) / 2 toward min.  One definition for the host (device_threshold)
+// and the device (k_finalize's speculative pass), so both build the same bits.
+__host__ __device__ inline void build_probe_tree(ProbeSet& ps, double t0, double mn, double mx) {
+  ps.T = kMaxProbes;
+  ps.t[0] = t0;
+  for (int k = 0; 2 * k + 2 < kMaxProbes; ++k) {
+    ps.t[2 * k + 1] = P_MUL(P_ADD(ps.t[k], mx), 0.5);
+    ps.t[2 * k + 2] = P_MUL(P_ADD(ps.t[k], mn), 0.5);
+  }
+}
+
+// Where k_finalize builds the speculative first pass of the next search
+// (the ProbeSet the probe kernel reads; nullptr = off).
+struct SpecProbe {
+  ProbeSet* dev = nullptr;
+  int64_t s_it = 0;  // the global batch size (the search's s_it)
+};
 struct ProbeScalars {
   double err_sum[kMaxProbes];  // sum err where candidate == 0 (discarded)
   double est_sum[kMaxProbes];  // sum est where candidate == 0
@@ -106,7 +126,15 @@ void launch_fold_one(cudaStream_t st, int64_t m, const double* x, const uint8_t*
 void launch_finalize(cudaStream_t st, int64_t nblk, int nq, const double* part,
                      const int64_t* cnt, int64_t* offsets, double* scratch, FoldScalars* out,
                      const unsigned long long* mm = nullptr, const double* err0 = nullptr,
-                     unsigned* ready = nullptr, unsigned seq = 0);
+                     unsigned* ready = nullptr, unsigned seq = 0,
+                     const SpecProbe& spec = SpecProbe{});
+
+// The speculative first pass: k_probe_multi + its trees with the ProbeSet
+// k_finalize left in device memory (both programmatic launches).
+void launch_probe_multi_dev(cudaStream_t st, int64_t m, const ProbeSet* dts, const double* est,
+                            const double* err, const uint8_t* flag, double* part, int64_t* cnt,
+                            double* scratch, ProbeScalars* out, unsigned* ready, unsigned seq,
+                            int* done);
 
 // T speculative probes in one pass + their trees; part [2][kMaxProbes][nblk],
 // cnt [kMaxProbes][nblk], scratch 2*3*kMaxProbes*nblk doubles.

@@ -575,3 +575,52 @@ def test_streamed_threshold_search_equals_exact_folds(pg, gpu, tmp_path):
         assert got[6] > 0  # threshold searches happened
         fallbacks += got[5]
     assert fallbacks <= 2  # the streamed passes decide (nearly) always
+
+
+def test_pipeline_switches_do_not_change_results(pg, gpu):
+    """The default launch pipeline -- deferred bisection (k_link + children
+    derived in k_evaluate) and programmatic dependent launches -- and the
+    opt-in speculative first probe pass queued behind k_finalize
+    (PAGANI_SPEC_PROBE=1) against the plain one (PAGANI_DEFER_BISECT=0
+    PAGANI_PDL=0: explicit split kernel, ordinary launches, every pass launched
+    by the host): the same trace bit for bit, including multi-pass searches
+    (f3) and failed ones."""
+    import json
+    import subprocess
+    import sys
+    cases = [(3, 8, 1e-3, True, 100), (6, 8, 1e-4, True, 60), (2, 8, 1e-3, True, 40),
+             (1, 8, 1e-3, False, 30), (4, 10, 1e-3, True, 10), (5, 5, 1e-4, True, 100)]
+
+    def row_key(r):
+        return [r.estimate.hex(), r.errorest.hex(), r.iterations, r.regions_generated,
+                str(r.status), [[row[k].hex() if isinstance(row[k], float) else row[k]
+                                 for k in sorted(row)] for row in r.trace]]
+
+    code = ("import json,sys; sys.path.insert(0, %r); import paper_2104_06494_b200 as pg\n"
+            "out=[]\n"
+            "for f,n,tau,relf,itm in %r:\n"
+            "    r=pg.integrate(pg.Integrand(f), pg.Bounds.unit_cube(n),"
+            " pg.Config(tau_rel=tau, rel_filtering_enabled=relf, it_max=itm), trace=True)\n"
+            "    out.append([r.estimate.hex(), r.errorest.hex(), r.iterations, r.regions_generated,"
+            " str(r.status), [[row[k].hex() if isinstance(row[k], float) else row[k]"
+            " for k in sorted(row)] for row in r.trace], r.spec_probe_passes])\n"
+            "print(json.dumps(out))\n") % (str(pg.__path__[0]).rsplit("/", 1)[0], cases)
+    def run(**sw):
+        env = dict(__import__("os").environ, **sw)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        return json.loads(p.stdout.strip().splitlines()[-1])
+
+    plain = run(PAGANI_DEFER_BISECT="0", PAGANI_PDL="0", PAGANI_SPEC_PROBE="0")
+    spec = run(PAGANI_SPEC_PROBE="1")  # the opt-in speculative first pass
+    spec_passes = 0
+    for (f, n, tau, relf, itm), got, sp in zip(cases, plain, spec):
+        assert got[6] == 0  # the plain pipeline never speculates
+        r = pg.integrate(pg.Integrand(f), pg.Bounds.unit_cube(n),
+                         pg.Config(tau_rel=tau, rel_filtering_enabled=relf, it_max=itm),
+                         trace=True)
+        assert row_key(r) == got[:6], (f, n, tau)
+        assert sp[:6] == got[:6], (f, n, tau, "speculative first pass")
+        spec_passes += sp[6]
+    assert spec_passes > 0  # the speculative pipeline did speculate
