@@ -1852,6 +1852,8 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
 // here: 10-18 B read per region, 16 B written per kept region, all coalesced.
 constexpr int kLinkThreads = 256;
 constexpr int kLinkPer = static_cast<int>(kBlock) / kLinkThreads;  // 8 consecutive regions
+// (__launch_bounds__(256, 5) -- 1.7 waves instead of 2.1 for a 1233-block
+// batch -- spilled and measured equal: 15.4 vs 15.2 us)
 __global__ void __launch_bounds__(kLinkThreads)
     k_link(int64_t m, const uint8_t* __restrict__ flag, int use_t, double t,
            const int64_t* __restrict__ offsets, const double* __restrict__ est,
