@@ -1852,36 +1852,33 @@ void launch_split(cudaStream_t st, int n, int64_t m, int64_t cap_src, int64_t ca
 // here: 10-18 B read per region, 16 B written per kept region, all coalesced.
 constexpr int kLinkThreads = 256;
 constexpr int kLinkPer = static_cast<int>(kBlock) / kLinkThreads;  // 8 consecutive regions
-// (__launch_bounds__(256, 5) -- 1.7 waves instead of 2.1 for a 1233-block
-// batch -- spilled and measured equal: 15.4 vs 15.2 us)
-__global__ void __launch_bounds__(kLinkThreads)
-    k_link(int64_t m, const uint8_t* __restrict__ flag, int use_t, double t,
-           const int64_t* __restrict__ offsets, const double* __restrict__ est,
-           const double* __restrict__ err, const uint8_t* __restrict__ axis,
-           uint64_t* __restrict__ link, double* __restrict__ pest) {
-  constexpr int W = kLinkThreads / 32;
-  __shared__ __align__(16) uint64_t s_link[kBlock];
-  __shared__ __align__(16) double s_pest[kBlock];
-  __shared__ int s_warp[W + 1];
-  pdl_trigger();  // the next k_evaluate may launch (it waits for this grid in pdl_wait)
-  const int64_t b = blockIdx.x;
+
+// One thread's 8 consecutive regions of a 2048-block, as loaded.
+struct LinkRegs {
+  uint2 fw, aw;  // flag / axis bytes
+  double2 xv[kLinkPer / 2], ev[kLinkPer / 2];
+};
+
+// every load issued before any use: flag / axis as 8-byte words, est / err
+// as 16-byte pairs (the block start is 2048-aligned, so all are aligned)
+__device__ __forceinline__ void link_load(LinkRegs& R, int64_t m, int64_t b,
+                                          const uint8_t* __restrict__ flag, int use_t,
+                                          const double* __restrict__ est,
+                                          const double* __restrict__ err,
+                                          const uint8_t* __restrict__ axis) {
   const int64_t base = b * kBlock;
   const int n = static_cast<int>(m - base < kBlock ? m - base : kBlock);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i0 = threadIdx.x * kLinkPer;  // this thread's 8 regions: base + i0 .. + 7
-  // every load issued before any use: flag / axis as 8-byte words, est / err
-  // as 16-byte pairs (the block start is 2048-aligned, so all are aligned)
-  uint2 fw = make_uint2(0u, 0u), aw = make_uint2(0u, 0u);
-  double2 xv[kLinkPer / 2], ev[kLinkPer / 2];
-  const bool full = i0 + kLinkPer <= n;
-  if (full) {
-    fw = __ldg(reinterpret_cast<const uint2*>(flag + base + i0));
-    aw = __ldg(reinterpret_cast<const uint2*>(axis + base + i0));
+  const int i0 = threadIdx.x * kLinkPer;
+  R.fw = make_uint2(0u, 0u);
+  R.aw = make_uint2(0u, 0u);
+  if (i0 + kLinkPer <= n) {
+    R.fw = __ldg(reinterpret_cast<const uint2*>(flag + base + i0));
+    R.aw = __ldg(reinterpret_cast<const uint2*>(axis + base + i0));
 #pragma unroll
     for (int u = 0; u < kLinkPer / 2; ++u) {
-      xv[u] = __ldg(reinterpret_cast<const double2*>(est + base + i0) + u);
-      ev[u] = use_t ? __ldg(reinterpret_cast<const double2*>(err + base + i0) + u)
-                    : make_double2(0.0, 0.0);
+      R.xv[u] = __ldg(reinterpret_cast<const double2*>(est + base + i0) + u);
+      R.ev[u] = use_t ? __ldg(reinterpret_cast<const double2*>(err + base + i0) + u)
+                      : make_double2(0.0, 0.0);
     }
   } else {  // the batch's ragged last block
     uint8_t fb[kLinkPer] = {}, ab[kLinkPer] = {};
@@ -1896,21 +1893,38 @@ __global__ void __launch_bounds__(kLinkThreads)
       }
 #pragma unroll
     for (int u = 0; u < kLinkPer; ++u) {
-      (u < 4 ? fw.x : fw.y) |= static_cast<unsigned>(fb[u]) << (8 * (u & 3));
-      (u < 4 ? aw.x : aw.y) |= static_cast<unsigned>(ab[u]) << (8 * (u & 3));
+      (u < 4 ? R.fw.x : R.fw.y) |= static_cast<unsigned>(fb[u]) << (8 * (u & 3));
+      (u < 4 ? R.aw.x : R.aw.y) |= static_cast<unsigned>(ab[u]) << (8 * (u & 3));
     }
 #pragma unroll
     for (int u = 0; u < kLinkPer / 2; ++u) {
-      xv[u] = make_double2(xs[2 * u], xs[2 * u + 1]);
-      ev[u] = make_double2(es[2 * u], es[2 * u + 1]);
+      R.xv[u] = make_double2(xs[2 * u], xs[2 * u + 1]);
+      R.ev[u] = make_double2(es[2 * u], es[2 * u + 1]);
     }
   }
-  // kept = flag && !(use_t && err < t) (classify.cpp:63-66)
+}
+
+struct LinkSmem {
+  uint64_t link[kBlock];
+  double pest[kBlock];
+  int warp[kLinkThreads / 32 + 1];
+};
+
+// kept = flag && !(use_t && err < t) (classify.cpp:63-66); the block's kept
+// regions in order, from rank offsets[b] on.  Ends with a barrier (S reusable).
+__device__ __forceinline__ void link_block(LinkSmem& S, const LinkRegs& R, int64_t b, int use_t,
+                                           double t, const int64_t* __restrict__ offsets,
+                                           uint64_t* __restrict__ link,
+                                           double* __restrict__ pest) {
+  constexpr int W = kLinkThreads / 32;
+  const int64_t base = b * kBlock;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i0 = threadIdx.x * kLinkPer;
   unsigned keep = 0;
 #pragma unroll
   for (int u = 0; u < kLinkPer; ++u) {
-    const unsigned f = ((u < 4 ? fw.x : fw.y) >> (8 * (u & 3))) & 0xffu;
-    const double e = (u & 1) ? ev[u / 2].y : ev[u / 2].x;
+    const unsigned f = ((u < 4 ? R.fw.x : R.fw.y) >> (8 * (u & 3))) & 0xffu;
+    const double e = (u & 1) ? R.ev[u / 2].y : R.ev[u / 2].x;
     keep |= (f != 0 && !(use_t && e < t)) ? (1u << u) : 0u;
   }
   // rank of the thread's first kept region in the block: warp scan + block scan
@@ -1921,36 +1935,85 @@ __global__ void __launch_bounds__(kLinkThreads)
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (lane == 31) s_warp[wid] = incl;
+  if (lane == 31) S.warp[wid] = incl;
   __syncthreads();
   if (threadIdx.x == 0) {
     int run = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      const int v = s_warp[w];
-      s_warp[w] = run;
+      const int v = S.warp[w];
+      S.warp[w] = run;
       run += v;
     }
-    s_warp[W] = run;
+    S.warp[W] = run;
   }
   __syncthreads();
-  int r = s_warp[wid] + incl - c;
+  int r = S.warp[wid] + incl - c;
   // stage the block's entries in rank order, then write them out coalesced
 #pragma unroll
   for (int u = 0; u < kLinkPer; ++u) {
     if (!((keep >> u) & 1u)) continue;
-    const unsigned ax = ((u < 4 ? aw.x : aw.y) >> (8 * (u & 3))) & 0xffu;
-    s_link[r] = static_cast<uint64_t>(base + i0 + u) | (static_cast<uint64_t>(ax) << 56);
-    s_pest[r] = (u & 1) ? xv[u / 2].y : xv[u / 2].x;
+    const unsigned ax = ((u < 4 ? R.aw.x : R.aw.y) >> (8 * (u & 3))) & 0xffu;
+    S.link[r] = static_cast<uint64_t>(base + i0 + u) | (static_cast<uint64_t>(ax) << 56);
+    S.pest[r] = (u & 1) ? R.xv[u / 2].y : R.xv[u / 2].x;
     ++r;
   }
   __syncthreads();
-  const int total = s_warp[W];
+  const int total = S.warp[W];
   const int64_t k0 = offsets[b];
   for (int i = threadIdx.x; i < total; i += kLinkThreads) {
-    link[k0 + i] = s_link[i];
-    pest[k0 + i] = s_pest[i];
+    link[k0 + i] = S.link[i];
+    pest[k0 + i] = S.pest[i];
   }
+  __syncthreads();
+}
+
+// One CTA per 2048-block.
+__global__ void __launch_bounds__(kLinkThreads)
+    k_link(int64_t m, const uint8_t* __restrict__ flag, int use_t, double t,
+           const int64_t* __restrict__ offsets, const double* __restrict__ est,
+           const double* __restrict__ err, const uint8_t* __restrict__ axis,
+           uint64_t* __restrict__ link, double* __restrict__ pest) {
+  __shared__ __align__(16) LinkSmem S;
+  pdl_trigger();  // the next k_evaluate may launch (it waits for this grid in pdl_wait)
+  LinkRegs R;
+  link_load(R, m, blockIdx.x, flag, use_t, est, err, axis);
+  link_block(S, R, blockIdx.x, use_t, t, offsets, link, pest);
+}
+
+// Persistent form: a grid of resident CTAs walks the blocks (b += gridDim.x)
+// with the next block's loads in flight while the current one is ranked and
+// written -- no wave tail, and the loads of block b + grid overlap block b's
+// scan / stores.
+__global__ void __launch_bounds__(kLinkThreads)
+    k_link_p(int64_t m, int64_t nblk, const uint8_t* __restrict__ flag, int use_t, double t,
+             const int64_t* __restrict__ offsets, const double* __restrict__ est,
+             const double* __restrict__ err, const uint8_t* __restrict__ axis,
+             uint64_t* __restrict__ link, double* __restrict__ pest) {
+  __shared__ __align__(16) LinkSmem S;
+  pdl_trigger();
+  int64_t b = blockIdx.x;
+  if (b >= nblk) return;
+  LinkRegs cur, nxt;
+  link_load(cur, m, b, flag, use_t, est, err, axis);
+  for (; b < nblk; b += gridDim.x) {
+    const int64_t bn = b + gridDim.x;
+    if (bn < nblk) link_load(nxt, m, bn, flag, use_t, est, err, axis);
+    link_block(S, cur, b, use_t, t, offsets, link, pest);
+    cur = nxt;
+  }
+}
+
+// PAGANI_LINK_PERSISTENT=1 selects k_link_p (measured slower on B200: 18.1
+// vs 15.2 us for a 1233-block f1 launch, 20.2 vs 18.1 ms per bench step --
+// 104 registers leave 2 CTAs per SM, and one CTA's serial scan / stage /
+// store per block is the critical path, not the loads).
+static bool link_persistent() {
+  static const bool on = [] {
+    const char* e = std::getenv("PAGANI_LINK_PERSISTENT");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
 }
 
 void launch_link(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, double t,
@@ -1958,6 +2021,19 @@ void launch_link(cudaStream_t st, int64_t m, const uint8_t* flag, int use_t, dou
                  const uint8_t* axis, uint64_t* link, double* pest) {
   const int64_t nblk = nblocks_of(m);
   if (nblk == 0) return;
+  if (link_persistent()) {
+    static const int slots = [] {
+      int d = 0, sms = 148, per = 1;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_link_p, kLinkThreads, 0);
+      return sms * (per > 0 ? per : 1);
+    }();
+    const int64_t g = nblk < slots ? nblk : slots;
+    k_link_p<<<static_cast<unsigned>(g), kLinkThreads, 0, st>>>(m, nblk, flag, use_t, t, offsets,
+                                                                est, err, axis, link, pest);
+    return;
+  }
   k_link<<<static_cast<unsigned>(nblk), kLinkThreads, 0, st>>>(m, flag, use_t, t, offsets, est,
                                                                err, axis, link, pest);
 }
