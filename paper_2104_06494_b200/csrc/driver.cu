@@ -2,18 +2,22 @@
 // makes every scalar decision exactly as /root/reference/proj/src/driver.cpp:83-215
 // does; the region list never leaves HBM.  Per iteration:
 //
-//   k_evaluate  (rule + integrand + 4th differences + two-level refine +
-//                rel-err classify, fused; its tail folds each 2048-block
-//                serially: partials of est, err, finished est/err, active
-//                counts, error min/max)
-//   k_finalize  (pairwise trees, kept offsets) -> 64 bytes into mapped host
-//                memory, a published sequence number (zero-copy hand-off)
+//   k_evaluate  (prologue: the deferred bisection -- region j's row derived
+//                from kept parent link[j >> 1] and stored; then rule +
+//                integrand + 4th differences + two-level refine + rel-err
+//                classify, fused; its tail folds each 2048-block serially:
+//                partials of est, err, finished est/err, active counts,
+//                error min/max)
+//   k_finalize  (pairwise trees, kept offsets; programmatic launch) -> 64
+//                bytes into mapped host memory, a published sequence number
+//                (zero-copy hand-off)
 //   -- host decisions --
 //   [threshold search: per pass k_probe_multi (15 speculative thresholds) ->
 //    k_finalize_multi -> 360 bytes zero-copy; the host replays the decisions]
-//   k_split_bulk (fused filter + bisect into the other buffer, TMA-staged rows)
-//   [sharded: allgathered block records before the trees, the boundary
-//    exchange after the split -- DESIGN.md 7]
+//   k_link      (the filter: link + parent estimate per kept region)
+//   [sharded: allgathered block records before the trees; k_split_bulk
+//    (fused filter + bisect, TMA-staged rows) and the boundary exchange
+//    after it -- DESIGN.md 7]
 //
 // Host arithmetic is compiled with -ffp-contract=off and uses the same
 // expression order as the reference, so v, e, v_f, e_f, budgets and
