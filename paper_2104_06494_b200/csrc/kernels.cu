@@ -633,6 +633,37 @@ __global__ void __launch_bounds__(256)
   publish();
 }
 
+// Exclusive block scan of one int64 per thread (NT = 1024 threads): warp
+// shuffles, the 32 warp totals scanned by warp 0 -- two barriers instead of
+// the 20 of a shared-memory Hillis-Steele scan.  `s` >= 33 entries; returns
+// the thread's exclusive prefix, *total the block's sum.
+__device__ __forceinline__ int64_t block_excl_scan_1024(int64_t local, int64_t* s,
+                                                        int64_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int64_t x = s[lane];
+    int64_t y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += v;
+    }
+    s[lane] = y - x;
+    if (lane == 31) s[32] = y;
+  }
+  __syncthreads();
+  *total = s[32];
+  return s[w] + incl - local;
+}
+
 // Exclusive scan of one count row (offsets of the accepted probe).
 __global__ void __launch_bounds__(1024) k_scan_counts(int64_t nblk, const int64_t* cnt,
                                                       int64_t* offsets) {
@@ -642,15 +673,8 @@ __global__ void __launch_bounds__(1024) k_scan_counts(int64_t nblk, const int64_
   const int64_t lo = tid * chunk, hi = lo + chunk < nblk ? lo + chunk : nblk;
   int64_t local = 0;
   for (int64_t i = lo; i < hi; ++i) local += cnt[i];
-  s_sum[tid] = local;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const int64_t v = tid >= off ? s_sum[tid - off] : 0;
-    __syncthreads();
-    s_sum[tid] += v;
-    __syncthreads();
-  }
-  int64_t run = s_sum[tid] - local;
+  int64_t total;
+  int64_t run = block_excl_scan_1024(local, s_sum, &total);
   for (int64_t i = lo; i < hi; ++i) {
     offsets[i] = run;
     run += cnt[i];
@@ -804,21 +828,15 @@ __global__ void __launch_bounds__(kFinThreads)
   const int64_t lo = tid * chunk, hi = lo + chunk < nblk ? lo + chunk : nblk;
   int64_t local = 0;
   for (int64_t i = lo; i < hi; ++i) local += cnt[i];
-  s_sum[tid] = local;
-  __syncthreads();
-  for (int off = 1; off < kFinThreads; off <<= 1) {
-    const int64_t v = tid >= off ? s_sum[tid - off] : 0;
-    __syncthreads();
-    s_sum[tid] += v;
-    __syncthreads();
-  }
-  int64_t run = s_sum[tid] - local;
+  static_assert(kFinThreads == 1024, "block_excl_scan_1024");
+  int64_t total;
+  int64_t run = block_excl_scan_1024(local, s_sum, &total);
   if (offsets)
     for (int64_t i = lo; i < hi; ++i) {
       offsets[i] = run;
       run += cnt[i];
     }
-  if (tid == kFinThreads - 1) out->count = s_sum[tid];
+  if (tid == kFinThreads - 1) out->count = total;
   signal_host(ready, seq);
   if (spec.dev && mm && tid == 0) {
     // after the host has its scalars: the next search's first pass, built
