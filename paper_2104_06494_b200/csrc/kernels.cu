@@ -158,6 +158,29 @@ __device__ __forceinline__ double tree_sum_smem(const double* src, int64_t n, do
   const double* s = src;
   double* d = sm;
   int64_t cur = n;
+  if (cur > 1) {  // first level from global memory: a thread's loads all in flight at once
+    constexpr int K = 8;
+    const int64_t half = cur / 2;
+    for (int64_t base = 0; base < half; base += static_cast<int64_t>(gn) * K) {
+      double a[K], b[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int64_t i = base + lt + static_cast<int64_t>(k) * gn;
+        a[k] = i < half ? s[2 * i] : 0.0;
+        b[k] = i < half ? s[2 * i + 1] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int64_t i = base + lt + static_cast<int64_t>(k) * gn;
+        if (i < half) d[i] = P_ADD(a[k], b[k]);
+      }
+    }
+    if ((cur & 1) && lt == 0) d[half] = s[cur - 1];
+    __syncthreads();
+    cur = half + (cur & 1);
+    s = d;
+    d += cur;
+  }
   while (cur > 1) {
     const int64_t half = cur / 2;
     for (int64_t i = lt; i < half; i += gn) d[i] = P_ADD(s[2 * i], s[2 * i + 1]);
@@ -757,9 +780,18 @@ __global__ void __launch_bounds__(kFinThreads)
   pdl_wait();  // the block records of the kernel before (launch_pdl)
   if (mm) {  // min_max of the errors from per-block keys (reduce.cpp:74-82; exact)
     unsigned long long a = ~0ULL, z = 0ULL;
-    for (int64_t i = tid; i < nblk; i += kFinThreads) {
-      a = mm[2 * i] < a ? mm[2 * i] : a;
-      z = mm[2 * i + 1] > z ? mm[2 * i + 1] : z;
+    for (int64_t b0 = 0; b0 < nblk; b0 += 4 * kFinThreads) {  // 4 key pairs in flight
+      ulonglong2 kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = b0 + tid + static_cast<int64_t>(u) * kFinThreads;
+        kk[u] = i < nblk ? reinterpret_cast<const ulonglong2*>(mm)[i] : make_ulonglong2(~0ULL, 0ULL);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a = kk[u].x < a ? kk[u].x : a;
+        z = kk[u].y > z ? kk[u].y : z;
+      }
     }
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, a, o);
@@ -827,6 +859,7 @@ __global__ void __launch_bounds__(kFinThreads)
   const int64_t chunk = (nblk + kFinThreads - 1) / kFinThreads;
   const int64_t lo = tid * chunk, hi = lo + chunk < nblk ? lo + chunk : nblk;
   int64_t local = 0;
+#pragma unroll 4
   for (int64_t i = lo; i < hi; ++i) local += cnt[i];
   static_assert(kFinThreads == 1024, "block_excl_scan_1024");
   int64_t total;
